@@ -1,0 +1,173 @@
+/*
+ * mprof_gpu.h — C ABI of the B200 matrix-profile engine (AAMP / p-norm AAMP / ACAMP).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference exposes a C++
+ * API (no C ABI); each entry point below replaces one reference symbol and keeps its
+ * argument meaning, validation order and error codes:
+ *
+ *   mprof_aamp        <- mprof::aamp        /root/reference/proj/include/mprof/aamp.hpp:59-60,
+ *                                           /root/reference/proj/src/aamp.cpp:7-15
+ *   mprof_aamp_pnorm  <- mprof::aamp_pnorm  /root/reference/proj/include/mprof/aamp.hpp:64-65,
+ *                                           /root/reference/proj/src/aamp.cpp:17-25
+ *   mprof_acamp       <- mprof::acamp       /root/reference/proj/include/mprof/acamp.hpp:100-102,
+ *                                           /root/reference/proj/src/acamp.cpp:29-36
+ *   mprof_validate    <- mprof::make_time_series + mprof::validate_config
+ *                                           /root/reference/proj/src/core.cpp:7-40
+ *   mprof_config_init <- mprof::ProfileConfig(m, kind) defaults
+ *                                           /root/reference/proj/include/mprof/core.hpp:78-93
+ *   mprof_sweep_device / mprof_finalize_device
+ *                     <- mprof::detail::run_engine split at its two phases (scan_diagonals,
+ *                        then the comparison->distance conversion)
+ *                                           /root/reference/proj/src/diag_scan.cpp:89-140
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary. Host entry points
+ * take HOST buffers (the series, and caller-allocated P/I of length n-m+1); *_device entry
+ * points take DEVICE pointers and run on the context's CUDA stream.
+ * There is no CPU fallback: without a CUDA device every compute call returns MPROF_E_CUDA.
+ */
+#ifndef MPROF_GPU_H
+#define MPROF_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPROF_GPU_ABI_VERSION 1
+
+/* Status codes. 1..13 are mprof::ErrorCode + 1 in declaration order
+ * (/root/reference/proj/include/mprof/core.hpp:16-30); >= 100 are device-side failures. */
+typedef enum mprof_status {
+  MPROF_OK = 0,
+  MPROF_E_NON_FINITE = 1,
+  MPROF_E_TOO_SHORT = 2,
+  MPROF_E_EMPTY_INPUT = 3,
+  MPROF_E_PARSE_ERROR = 4,
+  MPROF_E_BAD_SUBSEQ_LEN = 5,
+  MPROF_E_BAD_P = 6,
+  MPROF_E_BAD_EXCLUSION = 7,
+  MPROF_E_BAD_THRESHOLD = 8,
+  MPROF_E_BAD_KIND = 9,
+  MPROF_E_OUT_OF_RANGE = 10,
+  MPROF_E_DEGENERATE = 11,
+  MPROF_E_INCOMPLETE_STATE = 12,
+  MPROF_E_IO = 13,
+  MPROF_E_CUDA = 100,
+  MPROF_E_OOM = 101,
+  MPROF_E_BAD_ARG = 102,
+  MPROF_E_TOO_LARGE = 103
+} mprof_status;
+
+/* mprof::DistanceFamily (core.hpp:64) */
+enum { MPROF_EUCLIDEAN = 0, MPROF_PNORM = 1, MPROF_ZNORMALIZED = 2 };
+/* mprof::DiagonalOrder (core.hpp:75) — accepted, result is order-independent */
+enum { MPROF_ORDER_ASCENDING = 0, MPROF_ORDER_RANDOM = 1 };
+/* mprof::AcampVariant (acamp.hpp:95) */
+enum { MPROF_ACAMP_SQUARED_DISTANCE = 0, MPROF_ACAMP_FSCORE = 1 };
+/* GPU-side additions */
+enum { MPROF_FP64 = 0, MPROF_FP32 = 1 };
+
+/* Mirrors mprof::ProfileConfig + DistanceKind (core.hpp:66-93), plus the GPU-only fields
+ * `precision` and `exact`. Use mprof_config_init for the reference defaults. */
+typedef struct mprof_config {
+  uint64_t m;                /* subsequence length */
+  int32_t family;            /* MPROF_EUCLIDEAN / MPROF_PNORM / MPROF_ZNORMALIZED */
+  int32_t order;             /* DiagonalOrder; ignored by the GPU sweep */
+  double p;                  /* p-norm exponent (PNorm only), >= 1 */
+  uint64_t exclusion;        /* minimum admissible |i - j|, default 1 */
+  uint64_t order_seed;       /* ignored */
+  uint64_t refresh_interval; /* incremental steps between direct recomputations, 0 = never */
+  double flat_threshold;     /* variance floor for z-normalization, default 1e-12*m */
+  int32_t precision;         /* MPROF_FP64 (default) or MPROF_FP32 */
+  int32_t exact;             /* 1: parity build — reference arithmetic (no FMA, clamp, runs
+                                aligned to refresh_interval) for bit-exact AAMP / p-norm */
+} mprof_config;
+
+/* Result-free metadata of one sweep (filled when the pointer is non-null). */
+typedef struct mprof_run_info {
+  uint64_t cells;            /* admissible cells swept = sum over diagonals of (L - k) */
+  uint64_t diagonals;        /* diagonals swept */
+  uint64_t tiles;            /* CTAs launched for the sweep kernel */
+  uint64_t rows_per_tile;    /* run length R of each tile (seeded directly at its start) */
+  uint32_t kernel_launches;  /* kernels launched by this call */
+  float sweep_ms;            /* CUDA-event time of the sweep kernel alone (0 if not timed) */
+} mprof_run_info;
+
+typedef struct mprof_ctx mprof_ctx;
+
+/* ---- metadata ---------------------------------------------------------------------------- */
+int32_t mprof_abi_version(void);
+const char* mprof_status_string(int32_t status);
+/* Thread-local message of the last failing call (empty if none). */
+const char* mprof_last_error(void);
+
+/* ---- configuration ----------------------------------------------------------------------- */
+/* ProfileConfig(m, kind) defaults: exclusion 1, ascending, seed 0, refresh 0,
+ * flat_threshold 1e-12*m, fp64, exact 0. */
+void mprof_config_init(mprof_config* cfg, uint64_t m, int32_t family, double p);
+/* make_time_series (NonFinite, TooShort) then validate_config (BadSubseqLen, BadP,
+ * BadExclusion, BadThreshold), in the reference's order. */
+int32_t mprof_validate(const double* t, uint64_t n, const mprof_config* cfg);
+/* Length of the profile, n - m + 1 (core.hpp:99). */
+uint64_t mprof_profile_length(uint64_t n, uint64_t m);
+
+/* ---- contexts ---------------------------------------------------------------------------- */
+/* A context owns one device's workspace and CUDA stream. ctx == NULL in the calls below means
+ * the calling thread's default context on the current device. */
+int32_t mprof_ctx_create(int32_t device, mprof_ctx** out);
+void mprof_ctx_destroy(mprof_ctx* ctx);
+/* Run the context's work on an external stream (cudaStream_t as void*); NULL = own stream. */
+int32_t mprof_ctx_set_stream(mprof_ctx* ctx, void* stream);
+/* Time the sweep kernel with CUDA events on the launching stream (fills sweep_ms). */
+int32_t mprof_ctx_set_timing(mprof_ctx* ctx, int32_t enabled);
+
+/* ---- reference entry points (host buffers) ------------------------------------------------ */
+/* P[L] and I[L], L = n - m + 1, caller-allocated. `threads` (reference: CPU workers) selects
+ * nothing on the GPU and is accepted for signature parity. */
+int32_t mprof_aamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                   double* P, int64_t* I, mprof_run_info* info);
+int32_t mprof_aamp_pnorm(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                         double* P, int64_t* I, mprof_run_info* info);
+int32_t mprof_acamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                    int32_t variant, double* P, int64_t* I, mprof_run_info* info);
+
+/* ---- device-resident pipeline ------------------------------------------------------------- */
+/* Sweeps diagonals k in [k_lo, k_hi) ∩ [exclusion, n - m] of series d_t (device, n doubles) and
+ * writes the partial profile in COMPARISON space: d_cmp[L] (double, +inf = untouched) and
+ * d_idx[L] (int64, -1 = untouched). k_lo = k_hi = 0 sweeps every admissible diagonal.
+ * Comparison spaces: Euclidean D^2; p-norm sum |x-y|^p; z-normalized 1 - Pearson correlation.
+ * Partial profiles of disjoint bands merge by the lexicographic (cmp, idx) minimum
+ * (MinBuffer::absorb, /root/reference/proj/src/detail/diag_scan.hpp:45-52). No validation of
+ * the series values is done here (the host entry points do it). */
+int32_t mprof_sweep_device(mprof_ctx* ctx, const double* d_t, uint64_t n, const mprof_config* cfg,
+                           uint64_t k_lo, uint64_t k_hi, double* d_cmp, int64_t* d_idx,
+                           mprof_run_info* info);
+/* Converts comparison values to distances (to_distance / f_to_dz,
+ * /root/reference/proj/src/detail/diag_scan.hpp:153-167): d_P[L] from d_cmp[L]; idx untouched. */
+int32_t mprof_finalize_device(mprof_ctx* ctx, const double* d_cmp, uint64_t L,
+                              const mprof_config* cfg, double* d_P);
+/* Lexicographic (cmp, idx) merge of two partial profiles in place into (d_cmp, d_idx):
+ * the fused peer-memory alternative to the two-pass ncclMin merge. d_other_* may be peer
+ * pointers (NVLink) when peer access is enabled. */
+int32_t mprof_merge_device(mprof_ctx* ctx, double* d_cmp, int64_t* d_idx,
+                           const double* d_other_cmp, const int64_t* d_other_idx, uint64_t L);
+
+/* ---- multi-GPU partition (host-side math, no device needed) ------------------------------ */
+/* Equal-area cut of the diagonal range [exclusion, n-m] into `parts` contiguous bands; writes
+ * parts+1 boundaries (cuts[0] = exclusion, cuts[parts] = n-m+1). Area(k) = L - k cells. */
+int32_t mprof_band_cuts(uint64_t n, uint64_t m, uint64_t exclusion, uint32_t parts,
+                        uint64_t* cuts);
+/* Cells of band [k_lo, k_hi): sum_{k} (L - k). */
+uint64_t mprof_band_cells(uint64_t n, uint64_t m, uint64_t k_lo, uint64_t k_hi);
+
+/* ---- measurement --------------------------------------------------------------------------- */
+/* Measured FP64 peak of the current device: independent DFMA chains on every SM, timed with
+ * CUDA events. Writes GFLOP/s (DFMA = 2 flops) and the kernel time. */
+int32_t mprof_fp64_peak(mprof_ctx* ctx, double* gflops, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPROF_GPU_H */

@@ -1,0 +1,416 @@
+"""B200-native exact matrix profiles (AAMP, p-norm AAMP, ACAMP) — Python mirror of the
+reference's ``mprof`` C++ API over the C ABI in ``include/mprof_gpu.h``.
+
+Names, argument order, defaults and error codes follow the reference
+(/root/reference/proj/include/mprof/{core,aamp,acamp}.hpp):
+
+    ts  = make_time_series(samples)                       # NonFinite / TooShort
+    cfg = ProfileConfig(m, DistanceKind.euclidean())      # exclusion=1, refresh_interval=0, ...
+    mp  = aamp(ts, cfg)                                   # MatrixProfile(distances, nn_index)
+    mp  = aamp_pnorm(ts, ProfileConfig(m, DistanceKind.pnorm(3.0)))
+    mp  = acamp(ts, ProfileConfig(m, DistanceKind.znormalized()), AcampVariant.FScore)
+
+All compute runs in ``libmprof_gpu.so`` on the GPU. There is no CPU fallback: importing works
+without a GPU, every compute call raises ``Error(ErrorCode.Cuda)`` if no device is usable, and a
+missing library raises ``ImportError`` at first use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "ErrorCode", "Error", "DistanceFamily", "DistanceKind", "DiagonalOrder", "AcampVariant",
+    "Precision", "ProfileConfig", "TimeSeries", "make_time_series", "validate_config",
+    "profile_length", "default_flat_threshold", "MatrixProfile", "RunInfo", "aamp",
+    "aamp_pnorm", "acamp", "sweep_device", "finalize_device", "merge_device", "band_cuts",
+    "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context",
+]
+
+LIB_PATH = Path(__file__).resolve().parent / "libmprof_gpu.so"
+
+
+class ErrorCode(enum.IntEnum):
+    """mprof::ErrorCode (core.hpp:16-30) + device-side codes; value = C-ABI status."""
+    NonFinite = 1
+    TooShort = 2
+    EmptyInput = 3
+    ParseError = 4
+    BadSubseqLen = 5
+    BadP = 6
+    BadExclusion = 7
+    BadThreshold = 8
+    BadKind = 9
+    OutOfRange = 10
+    Degenerate = 11
+    IncompleteState = 12
+    Io = 13
+    Cuda = 100
+    OutOfMemory = 101
+    BadArgument = 102
+    TooLarge = 103
+
+
+class Error(RuntimeError):
+    """mprof::Error (core.hpp:32-44)."""
+
+    def __init__(self, code: ErrorCode, message: str, line: int = 0):
+        super().__init__(message)
+        self.code = code
+        self.line = line
+
+
+class DistanceFamily(enum.IntEnum):
+    Euclidean = 0
+    PNorm = 1
+    ZNormalized = 2
+
+
+@dataclass(frozen=True)
+class DistanceKind:
+    """mprof::DistanceKind (core.hpp:66-73)."""
+    family: DistanceFamily = DistanceFamily.Euclidean
+    p: float = 2.0
+
+    @staticmethod
+    def euclidean() -> "DistanceKind":
+        return DistanceKind(DistanceFamily.Euclidean, 2.0)
+
+    @staticmethod
+    def pnorm(p: float) -> "DistanceKind":
+        return DistanceKind(DistanceFamily.PNorm, float(p))
+
+    @staticmethod
+    def znormalized() -> "DistanceKind":
+        return DistanceKind(DistanceFamily.ZNormalized, 2.0)
+
+
+class DiagonalOrder(enum.IntEnum):
+    Ascending = 0
+    RandomPermutation = 1
+
+
+class AcampVariant(enum.IntEnum):
+    """mprof::AcampVariant (acamp.hpp:95)."""
+    SquaredDistance = 0
+    FScore = 1
+
+
+class Precision(enum.IntEnum):
+    FP64 = 0
+    FP32 = 1
+
+
+def default_flat_threshold(m: int) -> float:
+    """core.hpp:78-80."""
+    return 1e-12 * float(m)
+
+
+class ProfileConfig:
+    """mprof::ProfileConfig (core.hpp:82-93) + GPU-only ``precision`` and ``exact``."""
+
+    def __init__(self, m: int, kind: DistanceKind):
+        self.m = int(m)
+        self.kind = kind
+        self.exclusion = 1
+        self.order = DiagonalOrder.Ascending
+        self.order_seed = 0
+        self.refresh_interval = 0
+        self.flat_threshold = default_flat_threshold(self.m)
+        self.precision = Precision.FP64
+        self.exact = False
+
+    def copy(self) -> "ProfileConfig":
+        c = ProfileConfig(self.m, self.kind)
+        c.__dict__.update(self.__dict__)
+        return c
+
+    def __repr__(self) -> str:
+        return f"ProfileConfig({self.__dict__})"
+
+
+class TimeSeries:
+    """Immutable validated series (core.hpp:47-59); build with make_time_series."""
+    __slots__ = ("_v",)
+
+    def __init__(self, values: np.ndarray, _token=None):
+        if _token is not _TOKEN:
+            raise TypeError("use make_time_series()")
+        self._v = values
+
+    def values(self) -> np.ndarray:
+        return self._v
+
+    def size(self) -> int:
+        return int(self._v.shape[0])
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def __getitem__(self, i):
+        return self._v[i]
+
+
+_TOKEN = object()
+
+
+def make_time_series(samples: Sequence[float]) -> TimeSeries:
+    """core.cpp:7-19: NonFinite (first offending sample) is checked before TooShort."""
+    v = np.ascontiguousarray(np.asarray(samples, dtype=np.float64).reshape(-1))
+    bad = np.flatnonzero(~np.isfinite(v))
+    if bad.size:
+        raise Error(ErrorCode.NonFinite, f"sample {int(bad[0])} is not finite")
+    if v.shape[0] < 2:
+        raise Error(ErrorCode.TooShort, f"time series needs at least 2 samples, got {v.shape[0]}")
+    v = v.copy()
+    v.setflags(write=False)
+    return TimeSeries(v, _TOKEN)
+
+
+def profile_length(n: int, m: int) -> int:
+    return n - m + 1
+
+
+@dataclass
+class MatrixProfile:
+    """mprof::MatrixProfile (core.hpp:101-108)."""
+    distances: np.ndarray
+    nn_index: np.ndarray
+    m: int = 0
+    kind: DistanceKind = field(default_factory=DistanceKind)
+    info: Optional["RunInfo"] = None
+
+    def size(self) -> int:
+        return int(self.distances.shape[0])
+
+    def __len__(self) -> int:
+        return self.size()
+
+
+# --------------------------------------------------------------------------------------------
+# ctypes binding
+
+class _Config(C.Structure):
+    _fields_ = [("m", C.c_uint64), ("family", C.c_int32), ("order", C.c_int32), ("p", C.c_double),
+                ("exclusion", C.c_uint64), ("order_seed", C.c_uint64),
+                ("refresh_interval", C.c_uint64), ("flat_threshold", C.c_double),
+                ("precision", C.c_int32), ("exact", C.c_int32)]
+
+
+class RunInfo(C.Structure):
+    _fields_ = [("cells", C.c_uint64), ("diagonals", C.c_uint64), ("tiles", C.c_uint64),
+                ("rows_per_tile", C.c_uint64), ("kernel_launches", C.c_uint32),
+                ("sweep_ms", C.c_float)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "mprof_abi_version": (C.c_int32, []),
+    "mprof_status_string": (C.c_char_p, [C.c_int32]),
+    "mprof_last_error": (C.c_char_p, []),
+    "mprof_config_init": (None, [C.POINTER(_Config), C.c_uint64, C.c_int32, C.c_double]),
+    "mprof_validate": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(_Config)]),
+    "mprof_profile_length": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "mprof_ctx_create": (C.c_int32, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "mprof_ctx_destroy": (None, [C.c_void_p]),
+    "mprof_ctx_set_stream": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "mprof_ctx_set_timing": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "mprof_aamp": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config), C.c_void_p,
+                               C.c_void_p, C.POINTER(RunInfo)]),
+    "mprof_aamp_pnorm": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                     C.c_void_p, C.c_void_p, C.POINTER(RunInfo)]),
+    "mprof_acamp": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config), C.c_int32,
+                                C.c_void_p, C.c_void_p, C.POINTER(RunInfo)]),
+    "mprof_sweep_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                       C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                       C.POINTER(RunInfo)]),
+    "mprof_finalize_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                          C.c_void_p]),
+    "mprof_merge_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_uint64]),
+    "mprof_band_cuts": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                                    C.POINTER(C.c_uint64)]),
+    "mprof_band_cells": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "mprof_fp64_peak": (C.c_int32, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads the in-tree libmprof_gpu.so (raises ImportError if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (the CUDA extension is required; there is no fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _raise(status: int) -> None:
+    if status != 0:
+        msg = lib().mprof_last_error().decode(errors="replace")
+        try:
+            code = ErrorCode(status)
+        except ValueError:
+            code = ErrorCode.Cuda
+        raise Error(code, msg)
+
+
+def _to_c(cfg: ProfileConfig) -> _Config:
+    c = _Config()
+    c.m = cfg.m
+    c.family = int(cfg.kind.family)
+    c.order = int(cfg.order)
+    c.p = float(cfg.kind.p)
+    c.exclusion = int(cfg.exclusion)
+    c.order_seed = int(cfg.order_seed)
+    c.refresh_interval = int(cfg.refresh_interval)
+    c.flat_threshold = float(cfg.flat_threshold)
+    c.precision = int(cfg.precision)
+    c.exact = 1 if cfg.exact else 0
+    return c
+
+
+def _check_int_fields(cfg: ProfileConfig) -> None:
+    # size_t fields: negative values would wrap; the reference's validate_config rejects them
+    if cfg.m < 1:
+        raise Error(ErrorCode.BadSubseqLen, f"subsequence length {cfg.m} < 1")
+    if cfg.exclusion < 1:
+        raise Error(ErrorCode.BadExclusion, f"exclusion {cfg.exclusion} < 1")
+
+
+def validate_config(ts: TimeSeries, cfg: ProfileConfig) -> ProfileConfig:
+    """core.cpp:21-40 (same order and codes)."""
+    _check_int_fields(cfg)
+    c = _to_c(cfg)
+    v = ts.values()
+    _raise(lib().mprof_validate(v.ctypes.data, v.shape[0], C.byref(c)))
+    return cfg
+
+
+class Context:
+    """One device's workspace + stream (mprof_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _raise(lib().mprof_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+
+    def set_stream(self, stream_ptr: int) -> None:
+        _raise(lib().mprof_ctx_set_stream(self.handle, C.c_void_p(stream_ptr)))
+
+    def set_timing(self, on: bool) -> None:
+        _raise(lib().mprof_ctx_set_timing(self.handle, 1 if on else 0))
+
+    def close(self) -> None:
+        if self.handle:
+            lib().mprof_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ctx_handle(ctx: Optional[Context]):
+    return None if ctx is None else ctx.handle
+
+
+def _run(fn_name: str, ts: TimeSeries, cfg: ProfileConfig, extra, ctx, progress) -> MatrixProfile:
+    _check_int_fields(cfg)
+    v = ts.values()
+    n = v.shape[0]
+    L = max(n - cfg.m + 1, 0)
+    P = np.empty(L, dtype=np.float64)
+    I = np.empty(L, dtype=np.int64)
+    info = RunInfo()
+    c = _to_c(cfg)
+    args = [_ctx_handle(ctx), v.ctypes.data, n, C.byref(c), *extra, P.ctypes.data, I.ctypes.data,
+            C.byref(info)]
+    _raise(getattr(lib(), fn_name)(*args))
+    if progress is not None:
+        # The sweep is one device launch: the observer fires once, at completion
+        # (diagonals_done == diagonals_total). Its return value cannot cancel finished work.
+        progress(int(info.diagonals), int(info.diagonals))
+    return MatrixProfile(P, I, cfg.m, cfg.kind, info)
+
+
+def aamp(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Callable] = None, threads: int = 0,
+         ctx: Optional[Context] = None) -> MatrixProfile:
+    """mprof::aamp (aamp.hpp:59-60). `threads` is accepted for signature parity."""
+    return _run("mprof_aamp", ts, cfg, [], ctx, progress)
+
+
+def aamp_pnorm(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Callable] = None,
+               threads: int = 0, ctx: Optional[Context] = None) -> MatrixProfile:
+    """mprof::aamp_pnorm (aamp.hpp:64-65)."""
+    return _run("mprof_aamp_pnorm", ts, cfg, [], ctx, progress)
+
+
+def acamp(ts: TimeSeries, cfg: ProfileConfig, variant: AcampVariant = AcampVariant.FScore,
+          progress: Optional[Callable] = None, threads: int = 0,
+          ctx: Optional[Context] = None) -> MatrixProfile:
+    """mprof::acamp (acamp.hpp:100-102)."""
+    return _run("mprof_acamp", ts, cfg, [int(variant)], ctx, progress)
+
+
+# --------------------------------------------------------------------------------------------
+# device-resident pipeline (pointers are raw device addresses, e.g. torch tensor.data_ptr())
+
+def sweep_device(d_t: int, n: int, cfg: ProfileConfig, k_lo: int, k_hi: int, d_cmp: int, d_idx: int,
+                 ctx: Optional[Context] = None) -> RunInfo:
+    info = RunInfo()
+    c = _to_c(cfg)
+    _raise(lib().mprof_sweep_device(_ctx_handle(ctx), C.c_void_p(d_t), n, C.byref(c), k_lo, k_hi,
+                                    C.c_void_p(d_cmp), C.c_void_p(d_idx), C.byref(info)))
+    return info
+
+
+def finalize_device(d_cmp: int, L: int, cfg: ProfileConfig, d_P: int,
+                    ctx: Optional[Context] = None) -> None:
+    c = _to_c(cfg)
+    _raise(lib().mprof_finalize_device(_ctx_handle(ctx), C.c_void_p(d_cmp), L, C.byref(c),
+                                       C.c_void_p(d_P)))
+
+
+def merge_device(d_cmp: int, d_idx: int, d_ocmp: int, d_oidx: int, L: int,
+                 ctx: Optional[Context] = None) -> None:
+    _raise(lib().mprof_merge_device(_ctx_handle(ctx), C.c_void_p(d_cmp), C.c_void_p(d_idx),
+                                    C.c_void_p(d_ocmp), C.c_void_p(d_oidx), L))
+
+
+def band_cuts(n: int, m: int, exclusion: int, parts: int) -> list:
+    """Equal-area diagonal bands [cuts[g], cuts[g+1]) for `parts` GPUs (host math only)."""
+    out = (C.c_uint64 * (parts + 1))()
+    _raise(lib().mprof_band_cuts(n, m, exclusion, parts, out))
+    return [int(x) for x in out]
+
+
+def band_cells(n: int, m: int, k_lo: int, k_hi: int) -> int:
+    return int(lib().mprof_band_cells(n, m, k_lo, k_hi))
+
+
+def fp64_peak(ctx: Optional[Context] = None) -> tuple:
+    """Measured DFMA-chain FP64 throughput of the current device: (GFLOP/s, ms)."""
+    g = C.c_double()
+    ms = C.c_float()
+    _raise(lib().mprof_fp64_peak(_ctx_handle(ctx), C.byref(g), C.byref(ms)))
+    return float(g.value), float(ms.value)

@@ -1,0 +1,772 @@
+// mprof_gpu.cu — host orchestration, auxiliary kernels and the C ABI (include/mprof_gpu.h).
+//
+// Pipeline of one sweep (replaces mprof::detail::run_engine,
+// /root/reference/proj/src/diag_scan.cpp:89-140):
+//   init_best -> operand prep (pairs / z-norm statistics) -> first-diagonal thresholds
+//   -> sweep_kernel (all tiles) -> [z-norm flat-pair rule] -> split to (cmp, idx)
+//   -> finalize (comparison value -> distance).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/mprof_gpu.h"
+#include "sweep.cuh"
+
+using namespace mpg;
+
+namespace {
+
+// ---- tile configuration (one instantiation for every family) -------------------------------
+constexpr int kD = 8;    // diagonals per thread
+constexpr int kT = 128;  // threads per CTA
+constexpr int kS = 64;   // rows per shared-memory stage
+constexpr int kK = kD * kT;
+
+thread_local std::string g_last_error;
+
+int32_t fail(int32_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int32_t cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky non-fatal state
+  return fail(e == cudaErrorMemoryAllocation ? MPROF_E_OOM : MPROF_E_CUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define CK(expr)                                       \
+  do {                                                 \
+    cudaError_t e__ = (expr);                          \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #expr); \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// auxiliary kernels
+
+__global__ void k_init_best(BestEntry* best, int L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
+    best[i] = BestEntry{kInfBits, kNoIdx};
+}
+
+// A[p] = (t[p], t[p+m]) for p in [0, L-1)
+__global__ void k_build_pairs(const double* __restrict__ t, double2* __restrict__ A, int L, int m) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L - 1; p += gridDim.x * blockDim.x)
+    A[p] = make_double2(t[p], t[p + m]);
+}
+
+// Per-window mean and inverse centred norm, two-pass (the well-conditioned form; the reference
+// derives var from running sums, acamp.hpp:42-47). Flat windows (population variance <=
+// flat_threshold, the reference's rule acamp.hpp:55-56 / oracle.cpp:81-84) get B = 0.
+__global__ void k_znorm_stats(const double* __restrict__ t, int L, int m, double flat_thr,
+                              double* __restrict__ mu, double* __restrict__ B) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < m; ++l) s += t[p + l];
+    const double mean = s / m;
+    double ss = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double d = t[p + l] - mean;
+      ss = fma(d, d, ss);
+    }
+    mu[p] = mean;
+    const double var = ss / m;
+    B[p] = (var <= flat_thr) ? 0.0 : 1.0 / sqrt(ss);
+  }
+}
+
+// A[p] = (df_p, dg_p) for the centred-covariance slide (see Znorm in sweep.cuh).
+__global__ void k_znorm_pairs(const double* __restrict__ t, const double* __restrict__ mu,
+                              double2* __restrict__ A, int L, int m) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L - 1; p += gridDim.x * blockDim.x) {
+    const double a = t[p], b = t[p + m];
+    A[p] = make_double2(0.5 * (b - a), (b - mu[p + 1]) + (a - mu[p]));
+  }
+}
+
+// Thresholds from the band's first diagonal k1: every cell (i, i+k1) evaluated directly and
+// merged exactly. These are genuine cells of the band, so the result is unchanged; they only
+// give the high-word filter near-final thresholds before the tiles start.
+template <class P>
+__global__ void k_first_diag(SweepParams prm, int k1) {
+  const int L = prm.L;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + k1 <= L - 1;
+       i += gridDim.x * blockDim.x) {
+    const int j = i + k1;
+    const double mui = P::kCenteredSeed ? prm.mu[i] : 0.0;
+    const double muj = P::kCenteredSeed ? prm.mu[j] : 0.0;
+    double acc = 0.0;
+    for (int l = 0; l < prm.m; ++l) acc = P::seed(acc, prm.t[i + l] - mui, prm.t[j + l], muj, prm.p);
+    const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
+    const unsigned long long vb =
+        (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+    offer(prm.best, i, vb, j);
+    offer(prm.best, j, vb, i);
+  }
+}
+
+// z-normalized flat-pair rule (f_value, /root/reference/proj/include/mprof/acamp.hpp:52-60):
+// two flat windows score the minimum possible value (distance 0), so a flat window's nearest
+// neighbour is the SMALLEST admissible flat window; the sweep scored every pair with a flat
+// side as corr = 0 (d = 1, distance sqrt(2m)), which is already right for flat rows without a
+// flat partner and for every non-flat row.
+constexpr int kChunk = 1024;
+__global__ void k_flat_chunk_min(const double* __restrict__ B, int L, int* __restrict__ cmin) {
+  __shared__ int sm[32];
+  const int c = blockIdx.x;
+  int best = INT_MAX;
+  for (int x = threadIdx.x; x < kChunk; x += blockDim.x) {
+    const int p = c * kChunk + x;
+    if (p < L && B[p] == 0.0) best = min(best, p);
+  }
+  for (int off = 16; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = (threadIdx.x < (blockDim.x >> 5)) ? sm[threadIdx.x] : INT_MAX;
+    for (int off = 16; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, off));
+    if (threadIdx.x == 0) cmin[c] = best;
+  }
+}
+
+// Smallest flat position in [lo, hi] using per-chunk minima (cmin) to skip chunks.
+__device__ int first_flat(const double* __restrict__ B, const int* __restrict__ cmin, int lo, int hi) {
+  if (hi < lo) return INT_MAX;
+  for (int c = lo / kChunk; c <= hi / kChunk; ++c) {
+    const int cm = cmin[c];
+    if (cm == INT_MAX) continue;
+    if (cm >= lo) return cm <= hi ? cm : INT_MAX;
+    const int x1 = min(hi, c * kChunk + kChunk - 1);  // first chunk only: scan from lo
+    for (int x = lo; x <= x1; ++x)
+      if (B[x] == 0.0) return x;
+  }
+  return INT_MAX;
+}
+
+// For every flat window i: partner = smallest flat f with |i - f| in the band [k_lo, k_hi)
+// (k_lo >= exclusion); if one exists the entry becomes (0, f).
+__global__ void k_flat_fix(const double* __restrict__ B, int L, int k_lo, int k_hi,
+                           const int* __restrict__ cmin, BestEntry* best) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    if (B[i] != 0.0) continue;
+    int f = first_flat(B, cmin, max(0, i - k_hi + 1), i - k_lo);
+    if (f == INT_MAX) f = first_flat(B, cmin, i + k_lo, min(L - 1, i + k_hi - 1));
+    if (f != INT_MAX) best[i] = BestEntry{0ull, static_cast<long long>(f)};
+  }
+}
+
+__global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__ cmp,
+                        int64_t* __restrict__ idx, int L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    const BestEntry e = best[i];
+    cmp[i] = __longlong_as_double(static_cast<long long>(e.v));
+    idx[i] = (e.v == kInfBits || e.idx == kNoIdx) ? -1 : e.idx;
+  }
+}
+
+// to_distance (/root/reference/proj/src/detail/diag_scan.hpp:153-167) and f_to_dz
+// (/root/reference/proj/include/mprof/acamp.hpp:86-91) for the GPU comparison spaces.
+__global__ void k_finalize(const double* __restrict__ cmp, double* __restrict__ P, int L, int family,
+                           double p, double m) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    const double v = cmp[i];
+    double out;
+    if (isinf(v)) {
+      out = v;
+    } else if (family == MPROF_EUCLIDEAN) {
+      out = sqrt(v);
+    } else if (family == MPROF_PNORM) {
+      out = (p == 1.0) ? v : (p == 2.0) ? sqrt(v) : pow(v, 1.0 / p);
+    } else {
+      const double dz2 = fmax(0.0, fmin(2.0 * m * v, 4.0 * m));
+      out = sqrt(dz2);
+    }
+    P[i] = out;
+  }
+}
+
+__global__ void k_merge(double* __restrict__ cmp, int64_t* __restrict__ idx,
+                        const double* __restrict__ ocmp, const int64_t* __restrict__ oidx, int L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    const double a = cmp[i], b = ocmp[i];
+    const int64_t ia = idx[i], ib = oidx[i];
+    if (b < a || (b == a && ib < ia)) {
+      cmp[i] = b;
+      idx[i] = ib;
+    }
+  }
+}
+
+__global__ void k_dfma_peak(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double b = 0.999999999, c = 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+      a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 12345.678) out[0] = s;  // never true; keeps the chains alive
+}
+
+int grid_for(long long work, int block = 256) {
+  long long g = (work + block - 1) / block;
+  return static_cast<int>(std::max(1LL, std::min(g, 148LL * 32)));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// context
+
+struct mprof_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int num_sms = 148;
+  // grow-only device workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // host-API staging
+  void* io = nullptr;
+  size_t io_bytes = 0;
+  // tile table cache
+  std::vector<int2> tiles_h;
+  int2* tiles_d = nullptr;
+  size_t tiles_cap = 0;
+  long long tiles_key[6] = {-1, -1, -1, -1, -1, -1};
+};
+
+namespace {
+
+int32_t ensure(void** p, size_t* have, size_t need) {
+  if (*have >= need) return MPROF_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  CK(cudaMalloc(p, need));
+  *have = need;
+  return MPROF_OK;
+}
+
+thread_local std::unordered_map<int, mprof_ctx*> g_default_ctx;
+
+int32_t resolve_ctx(mprof_ctx* in, mprof_ctx** out) {
+  if (in) {
+    CK(cudaSetDevice(in->device));
+    *out = in;
+    return MPROF_OK;
+  }
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  auto it = g_default_ctx.find(dev);
+  if (it != g_default_ctx.end()) {
+    *out = it->second;
+    return MPROF_OK;
+  }
+  mprof_ctx* c = nullptr;
+  const int32_t st = mprof_ctx_create(dev, &c);
+  if (st != MPROF_OK) return st;
+  g_default_ctx[dev] = c;
+  *out = c;
+  return MPROF_OK;
+}
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct Workspace {
+  double2* A;
+  double* B;
+  double* mu;
+  BestEntry* best;
+  int* cmin;
+};
+
+int32_t carve(mprof_ctx* c, int L, Workspace* w) {
+  const size_t nA = align_up(sizeof(double2) * (size_t)L);
+  const size_t nB = align_up(sizeof(double) * (size_t)L);
+  const size_t nBest = align_up(sizeof(BestEntry) * (size_t)L);
+  const size_t nC = align_up(sizeof(int) * ((size_t)L / kChunk + 2));
+  const int32_t st = ensure(&c->ws, &c->ws_bytes, nA + 2 * nB + nBest + nC);
+  if (st != MPROF_OK) return st;
+  char* base = static_cast<char*>(c->ws);
+  w->A = reinterpret_cast<double2*>(base);
+  w->B = reinterpret_cast<double*>(base + nA);
+  w->mu = reinterpret_cast<double*>(base + nA + nB);
+  w->best = reinterpret_cast<BestEntry*>(base + nA + 2 * nB);
+  w->cmin = reinterpret_cast<int*>(base + nA + 2 * nB + nBest);
+  return MPROF_OK;
+}
+
+// rows-per-tile choice: exact mode aligns runs to refresh_interval (bit-exact reseeding points,
+// diag_scan.hpp:97-104) or runs whole diagonals; the fast mode balances seeding cost (m/(2R) of
+// the cell work) against having enough tiles for every SM.
+long long count_tiles(int L, int k_lo, int k_hi, long long R) {
+  long long t = 0;
+  for (long long kb = k_lo; kb < k_hi; kb += kK) t += (L - kb + R - 1) / R;
+  return t;
+}
+
+long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int num_sms) {
+  if (cfg->exact) {
+    if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
+    return L;  // the whole diagonal is one run, like the reference's refresh = 0
+  }
+  long long R = std::max<long long>(16LL * (long long)cfg->m, 8LL * kS);
+  R = (R + kS - 1) / kS * kS;
+  const long long want = 16LL * num_sms;
+  while (R > 2 * kS && count_tiles(L, k_lo, k_hi, R) < want) R = std::max<long long>(2 * kS, (R / 2 + kS - 1) / kS * kS);
+  if (cfg->refresh_interval > 0) R = std::min<long long>(R, (long long)cfg->refresh_interval);
+  return R;
+}
+
+int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, long long R, long long* ntiles) {
+  const long long key[6] = {L, k_lo, k_hi, R, kK, 1};
+  if (std::equal(key, key + 6, c->tiles_key)) {
+    *ntiles = (long long)c->tiles_h.size();
+    return MPROF_OK;
+  }
+  c->tiles_h.clear();
+  for (long long kb = k_lo; kb < k_hi; kb += kK)
+    for (long long ra = 0; ra < L - kb; ra += R) c->tiles_h.push_back(make_int2((int)kb, (int)ra));
+  const size_t need = c->tiles_h.size() * sizeof(int2);
+  void* p = c->tiles_d;
+  int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
+  c->tiles_d = static_cast<int2*>(p);
+  if (st != MPROF_OK) return st;
+  CK(cudaMemcpyAsync(c->tiles_d, c->tiles_h.data(), need, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // tiles_h may be rebuilt by the next call
+  std::copy(key, key + 6, c->tiles_key);
+  *ntiles = (long long)c->tiles_h.size();
+  return MPROF_OK;
+}
+
+template <class P>
+int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int k1,
+                     bool first_diag, uint32_t* launches, float* ms) {
+  using SB = StageBuf<P::kHasB, kD, kT, kS>;
+  const size_t smem = 2 * sizeof(SB);
+  auto kern = sweep_kernel<P, kD, kT, kS>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (first_diag && k1 <= prm.L - 1) {
+    k_first_diag<P><<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);
+    CK(cudaGetLastError());
+    ++*launches;
+  }
+  if (ntiles > INT_MAX) return fail(MPROF_E_TOO_LARGE, "too many tiles");
+  if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
+  kern<<<(unsigned)ntiles, kT, smem, c->stream>>>(prm);
+  CK(cudaGetLastError());
+  ++*launches;
+  if (c->timing) {
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaEventSynchronize(c->ev1));
+    CK(cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  }
+  return MPROF_OK;
+}
+
+int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
+                       long long ntiles, int k1, uint32_t* launches, float* ms) {
+  const bool fd = !cfg->exact;
+  if (cfg->family == MPROF_ZNORMALIZED)
+    return launch_sweep<Znorm>(c, prm, ntiles, k1, fd, launches, ms);
+  const bool pn = cfg->family == MPROF_PNORM;
+  const double p = cfg->p;
+  if (!pn || p == 2.0) {
+    return cfg->exact ? launch_sweep<Euclid<true>>(c, prm, ntiles, k1, fd, launches, ms)
+                      : launch_sweep<Euclid<false>>(c, prm, ntiles, k1, fd, launches, ms);
+  }
+  if (p == 1.0)
+    return cfg->exact ? launch_sweep<Pnorm<1, true>>(c, prm, ntiles, k1, fd, launches, ms)
+                      : launch_sweep<Pnorm<1, false>>(c, prm, ntiles, k1, fd, launches, ms);
+  if (p == 3.0)
+    return cfg->exact ? launch_sweep<Pnorm<3, true>>(c, prm, ntiles, k1, fd, launches, ms)
+                      : launch_sweep<Pnorm<3, false>>(c, prm, ntiles, k1, fd, launches, ms);
+  if (p == 4.0)
+    return cfg->exact ? launch_sweep<Pnorm<4, true>>(c, prm, ntiles, k1, fd, launches, ms)
+                      : launch_sweep<Pnorm<4, false>>(c, prm, ntiles, k1, fd, launches, ms);
+  return cfg->exact ? launch_sweep<Pnorm<0, true>>(c, prm, ntiles, k1, fd, launches, ms)
+                    : launch_sweep<Pnorm<0, false>>(c, prm, ntiles, k1, fd, launches, ms);
+}
+
+int32_t check_config(uint64_t n, const mprof_config* cfg) {
+  // validate_config (/root/reference/proj/src/core.cpp:21-40), same order and codes
+  if (cfg->m < 1 || cfg->m > n - 1)
+    return fail(MPROF_E_BAD_SUBSEQ_LEN, "subsequence length %llu outside [1, %llu] for series of length %llu",
+                (unsigned long long)cfg->m, (unsigned long long)(n - 1), (unsigned long long)n);
+  if (cfg->family == MPROF_PNORM && !(cfg->p >= 1.0))
+    return fail(MPROF_E_BAD_P, "p-norm exponent must be >= 1, got %f", cfg->p);
+  if (cfg->exclusion < 1 || cfg->exclusion > n - cfg->m)
+    return fail(MPROF_E_BAD_EXCLUSION, "exclusion %llu outside [1, %llu]",
+                (unsigned long long)cfg->exclusion, (unsigned long long)(n - cfg->m));
+  if (!(cfg->flat_threshold >= 0.0)) return fail(MPROF_E_BAD_THRESHOLD, "flat_threshold must be >= 0");
+  if (cfg->family < 0 || cfg->family > 2) return fail(MPROF_E_BAD_ARG, "unknown distance family %d", cfg->family);
+  if (cfg->precision != MPROF_FP64 && cfg->precision != MPROF_FP32)
+    return fail(MPROF_E_BAD_ARG, "unknown precision %d", cfg->precision);
+  if (n >= (uint64_t)INT_MAX - 2 * (uint64_t)kK) return fail(MPROF_E_TOO_LARGE, "series too long for 32-bit positions");
+  return MPROF_OK;
+}
+
+int32_t check_series(const double* t, uint64_t n) {
+  // make_time_series (/root/reference/proj/src/core.cpp:7-19): NonFinite first, then TooShort
+  for (uint64_t i = 0; i < n; ++i)
+    if (!std::isfinite(t[i])) return fail(MPROF_E_NON_FINITE, "sample %llu is not finite", (unsigned long long)i);
+  if (n < 2) return fail(MPROF_E_TOO_SHORT, "time series needs at least 2 samples, got %llu", (unsigned long long)n);
+  return MPROF_OK;
+}
+
+int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_config* cfg,
+                   uint64_t k_lo64, uint64_t k_hi64, double* d_cmp, int64_t* d_idx,
+                   mprof_run_info* info) {
+  int32_t st = check_config(n64, cfg);
+  if (st != MPROF_OK) return st;
+  if (cfg->precision == MPROF_FP32) return fail(MPROF_E_BAD_ARG, "FP32 mode not built yet");
+  const int n = (int)n64, m = (int)cfg->m;
+  const int L = n - m + 1;
+  // band: [max(k_lo, excl), min(k_hi, L)) ; 0,0 = everything
+  long long k_lo = (long long)cfg->exclusion, k_hi = L;
+  if (!(k_lo64 == 0 && k_hi64 == 0)) {
+    k_lo = std::max<long long>(k_lo, (long long)k_lo64);
+    k_hi = std::min<long long>(k_hi, (long long)k_hi64);
+  }
+  Workspace w;
+  st = carve(c, L, &w);
+  if (st != MPROF_OK) return st;
+  uint32_t launches = 0;
+  const int g = grid_for(L);
+  k_init_best<<<g, 256, 0, c->stream>>>(w.best, L);
+  ++launches;
+  const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  if (zn) {
+    k_znorm_stats<<<g, 256, 0, c->stream>>>(d_t, L, m, cfg->flat_threshold, w.mu, w.B);
+    k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
+    launches += 2;
+  } else {
+    k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m);
+    ++launches;
+  }
+  CK(cudaGetLastError());
+  float ms = 0.f;
+  long long ntiles = 0, R = 0;
+  unsigned long long cells = 0;
+  if (k_lo < k_hi) {
+    R = choose_R(cfg, L, (int)k_lo, (int)k_hi, c->num_sms);
+    st = build_tiles(c, L, (int)k_lo, (int)k_hi, R, &ntiles);
+    if (st != MPROF_OK) return st;
+    SweepParams prm;
+    prm.t = d_t;
+    prm.A = w.A;
+    prm.B = w.B;
+    prm.mu = w.mu;
+    prm.best = w.best;
+    prm.tiles = c->tiles_d;
+    prm.n = n;
+    prm.m = m;
+    prm.L = L;
+    prm.k_hi = (int)k_hi;
+    prm.R = (int)std::min<long long>(R, INT_MAX);
+    prm.p = cfg->p;
+    st = dispatch_sweep(c, cfg, prm, ntiles, (int)k_lo, &launches, &ms);
+    if (st != MPROF_OK) return st;
+    if (zn) {
+      const int nch = (L + kChunk - 1) / kChunk;
+      k_flat_chunk_min<<<nch, 256, 0, c->stream>>>(w.B, L, w.cmin);
+      k_flat_fix<<<g, 256, 0, c->stream>>>(w.B, L, (int)k_lo, (int)k_hi, w.cmin, w.best);
+      launches += 2;
+      CK(cudaGetLastError());
+    }
+    cells = mprof_band_cells(n64, cfg->m, (uint64_t)k_lo, (uint64_t)k_hi);
+  }
+  k_split<<<g, 256, 0, c->stream>>>(w.best, d_cmp, d_idx, L);
+  ++launches;
+  CK(cudaGetLastError());
+  if (info) {
+    info->cells = cells;
+    info->diagonals = k_hi > k_lo ? (uint64_t)(k_hi - k_lo) : 0;
+    info->tiles = (uint64_t)ntiles;
+    info->rows_per_tile = (uint64_t)R;
+    info->kernel_launches = launches;
+    info->sweep_ms = ms;
+  }
+  return MPROF_OK;
+}
+
+int32_t host_entry(mprof_ctx* in, const double* t, uint64_t n, const mprof_config* cfg,
+                   int32_t family_required, double* P, int64_t* I, mprof_run_info* info) {
+  if (!t || !cfg || !P || !I) return fail(MPROF_E_BAD_ARG, "null argument");
+  int32_t st = check_series(t, n);
+  if (st != MPROF_OK) return st;
+  st = check_config(n, cfg);
+  if (st != MPROF_OK) return st;
+  if (cfg->family != family_required) {
+    static const char* msg[] = {"aamp computes Euclidean profiles only",
+                                "aamp_pnorm requires a p-norm distance kind",
+                                "acamp requires the z-normalized distance kind"};
+    return fail(MPROF_E_BAD_KIND, "%s", msg[family_required]);
+  }
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  const uint64_t L = n - cfg->m + 1;
+  const size_t nt = align_up(n * sizeof(double)), nl = align_up(L * sizeof(double));
+  st = ensure(&c->io, &c->io_bytes, nt + 3 * nl);
+  if (st != MPROF_OK) return st;
+  char* base = static_cast<char*>(c->io);
+  double* d_t = reinterpret_cast<double*>(base);
+  double* d_cmp = reinterpret_cast<double*>(base + nt);
+  int64_t* d_idx = reinterpret_cast<int64_t*>(base + nt + nl);
+  double* d_P = reinterpret_cast<double*>(base + nt + 2 * nl);
+  CK(cudaMemcpyAsync(d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  st = sweep_impl(c, d_t, n, cfg, 0, 0, d_cmp, d_idx, info);
+  if (st != MPROF_OK) return st;
+  st = mprof_finalize_device(c, d_cmp, L, cfg, d_P);
+  if (st != MPROF_OK) return st;
+  if (info) info->kernel_launches += 1;
+  CK(cudaMemcpyAsync(P, d_P, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(I, d_idx, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return MPROF_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int32_t mprof_abi_version(void) { return MPROF_GPU_ABI_VERSION; }
+
+const char* mprof_status_string(int32_t s) {
+  switch (s) {
+    case MPROF_OK: return "ok";
+    case MPROF_E_NON_FINITE: return "NonFinite";
+    case MPROF_E_TOO_SHORT: return "TooShort";
+    case MPROF_E_EMPTY_INPUT: return "EmptyInput";
+    case MPROF_E_PARSE_ERROR: return "ParseError";
+    case MPROF_E_BAD_SUBSEQ_LEN: return "BadSubseqLen";
+    case MPROF_E_BAD_P: return "BadP";
+    case MPROF_E_BAD_EXCLUSION: return "BadExclusion";
+    case MPROF_E_BAD_THRESHOLD: return "BadThreshold";
+    case MPROF_E_BAD_KIND: return "BadKind";
+    case MPROF_E_OUT_OF_RANGE: return "OutOfRange";
+    case MPROF_E_DEGENERATE: return "Degenerate";
+    case MPROF_E_INCOMPLETE_STATE: return "IncompleteState";
+    case MPROF_E_IO: return "Io";
+    case MPROF_E_CUDA: return "Cuda";
+    case MPROF_E_OOM: return "OutOfMemory";
+    case MPROF_E_BAD_ARG: return "BadArgument";
+    case MPROF_E_TOO_LARGE: return "TooLarge";
+    default: return "unknown";
+  }
+}
+
+const char* mprof_last_error(void) { return g_last_error.c_str(); }
+
+void mprof_config_init(mprof_config* cfg, uint64_t m, int32_t family, double p) {
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->m = m;
+  cfg->family = family;
+  cfg->p = (family == MPROF_PNORM) ? p : 2.0;
+  cfg->exclusion = 1;
+  cfg->order = MPROF_ORDER_ASCENDING;
+  cfg->order_seed = 0;
+  cfg->refresh_interval = 0;
+  cfg->flat_threshold = 1e-12 * (double)m;  // default_flat_threshold (core.hpp:78-80)
+  cfg->precision = MPROF_FP64;
+  cfg->exact = 0;
+}
+
+int32_t mprof_validate(const double* t, uint64_t n, const mprof_config* cfg) {
+  if (!t || !cfg) return fail(MPROF_E_BAD_ARG, "null argument");
+  int32_t st = check_series(t, n);
+  if (st != MPROF_OK) return st;
+  return check_config(n, cfg);
+}
+
+uint64_t mprof_profile_length(uint64_t n, uint64_t m) { return n - m + 1; }
+
+int32_t mprof_ctx_create(int32_t device, mprof_ctx** out) {
+  if (!out) return fail(MPROF_E_BAD_ARG, "null out");
+  *out = nullptr;
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(MPROF_E_CUDA, "no CUDA device %d (%d present)", device, count);
+  CK(cudaSetDevice(device));
+  mprof_ctx* c = new mprof_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaStreamCreate"); }
+  c->own_stream = true;
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+  *out = c;
+  return MPROF_OK;
+}
+
+void mprof_ctx_destroy(mprof_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->ws) cudaFree(c->ws);
+  if (c->io) cudaFree(c->io);
+  if (c->tiles_d) cudaFree(c->tiles_d);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  for (auto it = g_default_ctx.begin(); it != g_default_ctx.end(); ++it)
+    if (it->second == c) { g_default_ctx.erase(it); break; }
+  delete c;
+}
+
+int32_t mprof_ctx_set_stream(mprof_ctx* in, void* stream) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  } else {
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  return MPROF_OK;
+}
+
+int32_t mprof_ctx_set_timing(mprof_ctx* in, int32_t enabled) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  c->timing = enabled != 0;
+  return MPROF_OK;
+}
+
+int32_t mprof_aamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg, double* P,
+                   int64_t* I, mprof_run_info* info) {
+  return host_entry(ctx, t, n, cfg, MPROF_EUCLIDEAN, P, I, info);
+}
+
+int32_t mprof_aamp_pnorm(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                         double* P, int64_t* I, mprof_run_info* info) {
+  return host_entry(ctx, t, n, cfg, MPROF_PNORM, P, I, info);
+}
+
+int32_t mprof_acamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                    int32_t variant, double* P, int64_t* I, mprof_run_info* info) {
+  if (variant != MPROF_ACAMP_FSCORE && variant != MPROF_ACAMP_SQUARED_DISTANCE)
+    return fail(MPROF_E_BAD_ARG, "unknown AcampVariant %d", variant);
+  // Both variants yield the same profile (acamp.hpp:93-95); the GPU compares in 1 - corr.
+  return host_entry(ctx, t, n, cfg, MPROF_ZNORMALIZED, P, I, info);
+}
+
+int32_t mprof_sweep_device(mprof_ctx* in, const double* d_t, uint64_t n, const mprof_config* cfg,
+                           uint64_t k_lo, uint64_t k_hi, double* d_cmp, int64_t* d_idx,
+                           mprof_run_info* info) {
+  if (!d_t || !cfg || !d_cmp || !d_idx) return fail(MPROF_E_BAD_ARG, "null argument");
+  if (n < 2) return fail(MPROF_E_TOO_SHORT, "time series needs at least 2 samples");
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  return sweep_impl(c, d_t, n, cfg, k_lo, k_hi, d_cmp, d_idx, info);
+}
+
+int32_t mprof_finalize_device(mprof_ctx* in, const double* d_cmp, uint64_t L, const mprof_config* cfg,
+                              double* d_P) {
+  if (!d_cmp || !cfg || !d_P) return fail(MPROF_E_BAD_ARG, "null argument");
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  k_finalize<<<grid_for((long long)L), 256, 0, c->stream>>>(d_cmp, d_P, (int)L, cfg->family, cfg->p,
+                                                           (double)cfg->m);
+  CK(cudaGetLastError());
+  return MPROF_OK;
+}
+
+int32_t mprof_merge_device(mprof_ctx* in, double* d_cmp, int64_t* d_idx, const double* d_ocmp,
+                           const int64_t* d_oidx, uint64_t L) {
+  if (!d_cmp || !d_idx || !d_ocmp || !d_oidx) return fail(MPROF_E_BAD_ARG, "null argument");
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  k_merge<<<grid_for((long long)L), 256, 0, c->stream>>>(d_cmp, d_idx, d_ocmp, d_oidx, (int)L);
+  CK(cudaGetLastError());
+  return MPROF_OK;
+}
+
+uint64_t mprof_band_cells(uint64_t n, uint64_t m, uint64_t k_lo, uint64_t k_hi) {
+  const uint64_t L = n - m + 1;
+  if (k_hi > L) k_hi = L;
+  if (k_lo >= k_hi) return 0;
+  // sum_{k=k_lo}^{k_hi-1} (L - k)
+  const uint64_t cnt = k_hi - k_lo;
+  const uint64_t first = L - k_lo, last = L - (k_hi - 1);
+  return (first + last) * cnt / 2;
+}
+
+int32_t mprof_band_cuts(uint64_t n, uint64_t m, uint64_t exclusion, uint32_t parts, uint64_t* cuts) {
+  if (!cuts || parts == 0) return fail(MPROF_E_BAD_ARG, "bad arguments");
+  if (m < 1 || m > n - 1) return fail(MPROF_E_BAD_SUBSEQ_LEN, "bad m");
+  if (exclusion < 1 || exclusion > n - m) return fail(MPROF_E_BAD_EXCLUSION, "bad exclusion");
+  const uint64_t L = n - m + 1;
+  const long double total = (long double)mprof_band_cells(n, m, exclusion, L);
+  cuts[0] = exclusion;
+  cuts[parts] = L;
+  uint64_t lo = exclusion;
+  for (uint32_t g = 1; g < parts; ++g) {
+    const long double target = total * g / parts;
+    // smallest K >= lo with cells(exclusion, K) >= target (binary search)
+    uint64_t a = lo, b = L;
+    while (a < b) {
+      const uint64_t mid = a + (b - a) / 2;
+      if ((long double)mprof_band_cells(n, m, exclusion, mid) >= target) b = mid; else a = mid + 1;
+    }
+    cuts[g] = a;
+    lo = a;
+  }
+  return MPROF_OK;
+}
+
+int32_t mprof_fp64_peak(mprof_ctx* in, double* gflops, float* ms_out) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  double* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(double)));
+  const int blocks = c->num_sms * 8, threads = 256, iters = 4096;
+  k_dfma_peak<<<blocks, threads, 0, c->stream>>>(d, 64);  // warm-up
+  CK(cudaEventRecord(c->ev0, c->stream));
+  k_dfma_peak<<<blocks, threads, 0, c->stream>>>(d, iters);
+  CK(cudaEventRecord(c->ev1, c->stream));
+  CK(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  cudaFree(d);
+  const double flops = 2.0 * 8 * 4 * (double)iters * blocks * threads;
+  if (gflops) *gflops = flops / (ms * 1e-3) / 1e9;
+  if (ms_out) *ms_out = ms;
+  return MPROF_OK;
+}
+
+}  // extern "C"
