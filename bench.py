@@ -1,0 +1,395 @@
+#!/usr/bin/env python3
+"""Benchmark of the matrix-profile hot path (BASELINE.json metric: matrix-profile cell updates/s
+at n = 2^20, 1/2/4/8 B200, and % of the FP64 roofline).
+
+Workload (BASELINE.json configs[3], "C4"): float64 random walk with a 5x-variance anomaly window,
+n = 2^20, m = 1024, exclusion 1, FP64. One STEP = the AAMP sweep and the ACAMP sweep of that
+series (both engines the north-star targets at n = 2^20), each: band sweep -> ncclMin merge
+(N > 1) -> finalize. Cells per engine = (n-m)(n-m+1)/2 (/root/reference/proj/src/bench.cpp:110).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref, compiled from
+/root/reference/proj/src; the C restatement oracle/ if _ref is absent) on the host cores, on a
+bounded sample of the same workload, and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "matrix-profile cell updates/sec at n=2^20 (1/2/4/8 B200) and % of FP64 roofline"
+UNIT = "cells/s"
+N_C4, M_C4 = 1 << 20, 1024
+# algorithmic FP64 flops per cell update (DFMA = 2 flops, compares not counted)
+FLOPS_PER_CELL = {"aamp": 6, "acamp": 8, "pnorm1": 4, "pnorm3": 8}
+CPU_SAMPLE_N = 1 << 17     # bounded CPU sample: first 2^17 samples of the same series, same m
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+DATA = ("synthetic: seeded float64 Gaussian random walk with one 500-step window of 5x step "
+        "variance (BASELINE.json configs[3]); n=2^20, m=1024")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--engines", default="aamp,acamp")
+    ap.add_argument("--n", type=int, default=N_C4)
+    ap.add_argument("--m", type=int, default=M_C4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def cells(n, m):
+    return (n - m) * (n - m + 1) // 2
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi DURING the timed region)
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+                power.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline: the reference's own implementation on the host cores (bounded sample)
+
+def cpu_baseline(t, m, engines, threads=None):
+    import oracle
+    threads = threads or (os.cpu_count() or 1)
+    sample = t[:CPU_SAMPLE_N]
+    kind = "reference" if oracle.ref_available() else "port"
+    total_cells, total_s = 0, 0.0
+    for e in engines:
+        fam = oracle.EUCLIDEAN if e == "aamp" else oracle.ZNORM
+        t0 = time.perf_counter()
+        if kind == "reference":
+            oracle.ref_profile(sample, m, fam, threads=threads)
+        else:
+            oracle.scan(sample, m, fam, threads=threads)
+        total_s += time.perf_counter() - t0
+        total_cells += cells(sample.size, m)
+    return {"value": total_cells / total_s, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{'+'.join(engines)} on the first {sample.size} samples of the same series, "
+                      f"m={m} ({total_cells:.3e} cells, {total_s:.2f} s wall, "
+                      f"{'oracle/_ref = reference C++ built -O3' if kind == 'reference' else 'oracle C restatement'})"}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_1901_05708_b200 import workloads as W
+    t = W.c4(n=args.n)
+    engines = args.engines.split(",")
+    import oracle
+    threads = os.cpu_count() or 1
+    kind = "reference" if oracle.ref_available() else "port"
+    sample = t[:CPU_SAMPLE_N]
+    step_cells = sum(cells(sample.size, args.m) for _ in engines)
+
+    def step():
+        for e in engines:
+            fam = oracle.EUCLIDEAN if e == "aamp" else oracle.ZNORM
+            if kind == "reference":
+                oracle.ref_profile(sample, args.m, fam, threads=threads)
+            else:
+                oracle.scan(sample, args.m, fam, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = step_cells * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": DATA,
+        "config": {"workload": f"C4 {'+'.join(engines)}: bounded CPU sample of the n=2^20 series "
+                               f"(first {sample.size} samples), m={args.m}, exclusion 1, FP64",
+                   "n": int(sample.size), "m": args.m, "engines": engines},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"first {sample.size} samples of the C4 series per engine per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+
+def load_traffic():
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text())
+        except Exception:
+            return None
+    return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_1901_05708_b200 as mp
+    from paper_1901_05708_b200 import workloads as W
+    from paper_1901_05708_b200.distributed import band_for_rank, merge_min_
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, m = args.n, args.m
+    L = n - m + 1
+    engines = args.engines.split(",")
+    t = W.c4(n=n)
+    ctx = mp.Context(local)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_timing(True)
+
+    cfgs = {"aamp": mp.ProfileConfig(m, mp.DistanceKind.euclidean()),
+            "acamp": mp.ProfileConfig(m, mp.DistanceKind.znormalized())}
+    band = band_for_rank(n, m, 1, rank, world)
+    with torch.cuda.stream(stream):
+        d_t = torch.tensor(t, dtype=torch.float64, device="cuda")
+        bufs = {e: (torch.empty(L, dtype=torch.float64, device="cuda"),
+                    torch.empty(L, dtype=torch.int64, device="cuda"),
+                    torch.empty(L, dtype=torch.float64, device="cuda")) for e in engines}
+        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    stream.synchronize()
+
+    sweep_ms = {e: [] for e in engines}
+    launches = [0]
+
+    def step(record=True):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between steps (inputs are L2-resident)
+            for e in engines:
+                cmp, idx, P = bufs[e]
+                info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], cmp.data_ptr(),
+                                       idx.data_ptr(), ctx=ctx)
+                if world > 1:
+                    merge_min_(cmp, idx)
+                mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
+                                   P.data_ptr(), ctx=ctx)
+                if record:
+                    sweep_ms[e].append(info.sweep_ms)
+                    launches[0] += info.kernel_launches + 1
+
+    for _ in range(args.warmup):
+        step(record=False)
+    for e in engines:
+        sweep_ms[e].clear()
+    launches[0] = 0
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        x = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        ms = float(x.item())
+    total_cells = cells(n, m) * len(engines)
+    value = total_cells * args.steps / (ms * 1e-3)
+
+    # roofline of the sweep kernels (the dominant kernels, >97% of the step): algorithmic FP64
+    # flops per launch / CUDA-event duration of the launch, against the FP64 peak measured live
+    # (DFMA chains on every SM).
+    peak_gflops, _ = mp.fp64_peak(ctx)
+    rank_cells = mp.band_cells(n, m, band[0], band[1])
+    per_engine = {}
+    flops_total, kern_s_total = 0.0, 0.0
+    for e in engines:
+        avg_ms = sum(sweep_ms[e]) / max(1, len(sweep_ms[e]))
+        fl = rank_cells * FLOPS_PER_CELL[e]
+        flops_total += fl
+        kern_s_total += avg_ms * 1e-3
+        per_engine[e] = {"sweep_ms": avg_ms, "cells_per_s_gpu": rank_cells / (avg_ms * 1e-3),
+                         "flops_per_cell": FLOPS_PER_CELL[e],
+                         "tflops": fl / (avg_ms * 1e-3) / 1e12,
+                         "frac_of_fp64_peak": fl / (avg_ms * 1e-3) / (peak_gflops * 1e9)}
+    achieved = flops_total / kern_s_total / 1e12
+    prof = load_traffic() or {}
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_gflops / 1e3,
+                "unit": "TFLOP/s", "frac": achieved * 1e3 / peak_gflops,
+                "traffic": prof.get("dram_bytes_per_launch"),
+                "peak_source": "measured live: mprof_fp64_peak (independent DFMA chains, 148 SMs, CUDA events)",
+                "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
+                "algorithmic_bytes_per_launch": 8 * n + 16 * L,
+                "note": "FP64-pipe bound (T and P/I are L2-resident: ~1e-4 B/cell); neither HBM nor tensor cores",
+                "per_engine": per_engine}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": {"workload": f"C4 {'+'.join(engines)}: n={n}, m={m}, exclusion 1, FP64, "
+                                   f"{'equal-area diagonal bands + ncclMin merge' if world > 1 else 'single GPU'}",
+                       "n": n, "m": m, "engines": engines, "cells_per_step": total_cells,
+                       "l2": "flushed every step (256 MiB memset inside the timed region)",
+                       "parallelism": f"diagonal-band dp{world}"},
+            "roofline": roofline, "gpu_launches": launches[0], "clocks": clk}
+
+    # end to end through the public API: pinned host series in, P and I back to the host
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx,
+                          stream)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(t, m, engines)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, stream):
+    import ctypes as C
+    L = n - m + 1
+    h_t = torch.from_numpy(t).pin_memory()
+    h_P = torch.empty(L, dtype=torch.float64).pin_memory()
+    h_I = torch.empty(L, dtype=torch.int64).pin_memory()
+    lib = mp.lib()
+    ccfg = {e: mp._to_c(cfgs[e]) for e in engines}
+
+    def one():
+        if world == 1:
+            for e in engines:
+                if e == "aamp":
+                    st = lib.mprof_aamp(ctx.handle, h_t.data_ptr(), n, C.byref(ccfg[e]), h_P.data_ptr(),
+                                        h_I.data_ptr(), None)
+                else:
+                    st = lib.mprof_acamp(ctx.handle, h_t.data_ptr(), n, C.byref(ccfg[e]), 1,
+                                         h_P.data_ptr(), h_I.data_ptr(), None)
+                assert st == 0, lib.mprof_last_error()
+        else:
+            with torch.cuda.stream(stream):
+                d_t = h_t.to("cuda", non_blocking=True)
+                for e in engines:
+                    cmp = torch.empty(L, dtype=torch.float64, device="cuda")
+                    idx = torch.empty(L, dtype=torch.int64, device="cuda")
+                    P = torch.empty(L, dtype=torch.float64, device="cuda")
+                    stream.synchronize()
+                    mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], cmp.data_ptr(),
+                                    idx.data_ptr(), ctx=ctx)
+                    merge_min = __import__("paper_1901_05708_b200.distributed",
+                                           fromlist=["merge_min_"]).merge_min_
+                    merge_min(cmp, idx)
+                    mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
+                                       P.data_ptr(), ctx=ctx)
+                    h_P.copy_(P, non_blocking=True)
+                    h_I.copy_(idx, non_blocking=True)
+                stream.synchronize()
+
+    one()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if world > 1:
+        x = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        el = float(x.item())
+    total = cells(n, m) * len(engines) * args.steps
+    return {"value": total / el, "unit": UNIT, "h2d_bytes_per_step": 8 * n * len(engines),
+            "d2h_bytes_per_step": 16 * L * len(engines),
+            "path": "C ABI host entry points mprof_aamp / mprof_acamp (pinned host buffers)"
+                    if world == 1 else "mprof_sweep_device + ncclMin merge + mprof_finalize_device, H2D/D2H pinned",
+            "ms_per_step": el / args.steps * 1e3}
+
+
+if __name__ == "__main__":
+    main()

@@ -143,10 +143,13 @@ int32_t mprof_acamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_con
 int32_t mprof_sweep_device(mprof_ctx* ctx, const double* d_t, uint64_t n, const mprof_config* cfg,
                            uint64_t k_lo, uint64_t k_hi, double* d_cmp, int64_t* d_idx,
                            mprof_run_info* info);
-/* Converts comparison values to distances (to_distance / f_to_dz,
- * /root/reference/proj/src/detail/diag_scan.hpp:153-167): d_P[L] from d_cmp[L]; idx untouched. */
-int32_t mprof_finalize_device(mprof_ctx* ctx, const double* d_cmp, uint64_t L,
-                              const mprof_config* cfg, double* d_P);
+/* Distances d_P[L] of a (merged) comparison-space profile of series d_t (n samples), the
+ * finalization of run_engine (to_distance / f_to_dz, /root/reference/proj/src/detail/diag_scan.hpp:
+ * 153-167). Default mode: the distance of each chosen pair (i, d_idx[i]) is recomputed directly
+ * (no sliding drift; exact zeros for identical z-normalized windows). exact = 1: the reference's
+ * conversion of the comparison value. Untouched entries (idx -1) stay +inf. */
+int32_t mprof_finalize_device(mprof_ctx* ctx, const double* d_t, uint64_t n, const double* d_cmp,
+                              const int64_t* d_idx, const mprof_config* cfg, double* d_P);
 /* Lexicographic (cmp, idx) merge of two partial profiles in place into (d_cmp, d_idx):
  * the fused peer-memory alternative to the two-pass ncclMin merge. d_other_* may be peer
  * pointers (NVLink) when peer access is enabled. */

@@ -3,6 +3,7 @@
 // with -Dmprof=mprof_ref so it can never collide with the drop-in's mprof:: symbols.
 // Exposes the reference's public entry points (aamp / aamp_pnorm / acamp / brute_profile and
 // run_engine's comparison values) behind plain C functions for ctypes.
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -16,6 +17,9 @@
 using namespace mprof;
 
 namespace {
+// sentinel for "keep ProfileConfig's default flat_threshold" (any other value is passed through,
+// including invalid ones, so validation parity can be tested)
+constexpr double kDefaultFlat = -7.0e300;
 int code_of(const Error& e) { return static_cast<int>(e.code()) + 1; }
 
 ProfileConfig make_cfg(uint64_t m, int family, double p, uint64_t excl, uint64_t refresh, double flat) {
@@ -25,7 +29,7 @@ ProfileConfig make_cfg(uint64_t m, int family, double p, uint64_t excl, uint64_t
   ProfileConfig cfg(m, kind);
   cfg.exclusion = excl;
   cfg.refresh_interval = refresh;
-  if (flat >= 0.0) cfg.flat_threshold = flat;
+  if (flat != kDefaultFlat) cfg.flat_threshold = flat;
   return cfg;
 }
 
@@ -37,7 +41,8 @@ void copy_out(const MatrixProfile& mp, double* P, int64_t* I) {
 
 extern "C" {
 
-// family 0 aamp, 1 aamp_pnorm, 2 acamp(variant: 1 FScore, 0 SquaredDistance). flat < 0: default.
+// family 0 aamp, 1 aamp_pnorm, 2 acamp(variant: 1 FScore, 0 SquaredDistance).
+// flat == -7e300: ProfileConfig's default.
 // Returns 0 or ErrorCode+1; -1 for any other exception.
 int ref_profile(const double* t, uint64_t n, uint64_t m, int family, double p, uint64_t excl,
                 uint64_t refresh, double flat, int variant, unsigned threads, double* P, int64_t* I) {

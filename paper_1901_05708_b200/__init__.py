@@ -233,8 +233,8 @@ EXPORTS = {
     "mprof_sweep_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
                                        C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                                        C.POINTER(RunInfo)]),
-    "mprof_finalize_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
-                                          C.c_void_p]),
+    "mprof_finalize_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                          C.c_void_p, C.POINTER(_Config), C.c_void_p]),
     "mprof_merge_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_uint64]),
     "mprof_band_cuts": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
@@ -384,11 +384,11 @@ def sweep_device(d_t: int, n: int, cfg: ProfileConfig, k_lo: int, k_hi: int, d_c
     return info
 
 
-def finalize_device(d_cmp: int, L: int, cfg: ProfileConfig, d_P: int,
+def finalize_device(d_t: int, n: int, d_cmp: int, d_idx: int, cfg: ProfileConfig, d_P: int,
                     ctx: Optional[Context] = None) -> None:
     c = _to_c(cfg)
-    _raise(lib().mprof_finalize_device(_ctx_handle(ctx), C.c_void_p(d_cmp), L, C.byref(c),
-                                       C.c_void_p(d_P)))
+    _raise(lib().mprof_finalize_device(_ctx_handle(ctx), C.c_void_p(d_t), n, C.c_void_p(d_cmp),
+                                       C.c_void_p(d_idx), C.byref(c), C.c_void_p(d_P)))
 
 
 def merge_device(d_cmp: int, d_idx: int, d_ocmp: int, d_oidx: int, L: int,

@@ -180,22 +180,57 @@ __global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__
 
 // to_distance (/root/reference/proj/src/detail/diag_scan.hpp:153-167) and f_to_dz
 // (/root/reference/proj/include/mprof/acamp.hpp:86-91) for the GPU comparison spaces.
-__global__ void k_finalize(const double* __restrict__ cmp, double* __restrict__ P, int L, int family,
-                           double p, double m) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+// One warp per entry. In the default mode the distance of the chosen pair (i, idx[i]) is
+// RECOMPUTED directly (O(m), two-pass z-normalization) instead of converting the running
+// comparison value: the sweep decides the argmin, the reported value carries no sliding drift
+// and near-duplicate z-normalized windows come out at ~1e-14 instead of sqrt(eps). Flat rules
+// as f_value / dist_znorm (acamp.hpp:52-57, oracle.cpp:81-84). In the exact (parity) mode the
+// reference's own conversion of the comparison value is applied.
+__global__ void k_finalize(const double* __restrict__ t, const double* __restrict__ cmp,
+                           const int64_t* __restrict__ idx, const double* __restrict__ mu,
+                           const double* __restrict__ B, double* __restrict__ P, int L, int m,
+                           int family, double p, int exact) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < L; i += warps) {
     const double v = cmp[i];
+    const long long j = idx[i];
+    const double md = (double)m;
     double out;
-    if (isinf(v)) {
+    if (isinf(v) || j < 0) {
       out = v;
-    } else if (family == MPROF_EUCLIDEAN) {
-      out = sqrt(v);
-    } else if (family == MPROF_PNORM) {
-      out = (p == 1.0) ? v : (p == 2.0) ? sqrt(v) : pow(v, 1.0 / p);
+    } else if (exact) {
+      if (family == MPROF_EUCLIDEAN) out = sqrt(v);
+      else if (family == MPROF_PNORM) out = (p == 1.0) ? v : (p == 2.0) ? sqrt(v) : pow(v, 1.0 / p);
+      else out = sqrt(fmax(0.0, fmin(2.0 * md * v, 4.0 * md)));
+    } else if (family == MPROF_ZNORMALIZED) {
+      const double bi = B[i], bj = B[j];
+      if (bi == 0.0 || bj == 0.0) {
+        out = (bi == 0.0 && bj == 0.0) ? 0.0 : sqrt(2.0 * md);
+      } else {
+        const double mi = mu[i], mj = mu[j];
+        double s = 0.0;
+        for (int l = lane; l < m; l += 32) {
+          const double d = (t[i + l] - mi) * bi - (t[j + l] - mj) * bj;
+          s = fma(d, d, s);
+        }
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        out = sqrt(fmin(md * s, 4.0 * md));
+      }
     } else {
-      const double dz2 = fmax(0.0, fmin(2.0 * m * v, 4.0 * m));
-      out = sqrt(dz2);
+      double s = 0.0;
+      for (int l = lane; l < m; l += 32) {
+        const double d = fabs(t[i + l] - t[j + l]);
+        if (family == MPROF_EUCLIDEAN || p == 2.0) s = fma(d, d, s);
+        else if (p == 1.0) s += d;
+        else if (p == 3.0) s = fma(d * d, d, s);
+        else if (p == 4.0) { const double d2 = d * d; s = fma(d2, d2, s); }
+        else s += pow(d, p);
+      }
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      out = (family == MPROF_EUCLIDEAN || p == 2.0) ? sqrt(s) : (p == 1.0) ? s : pow(s, 1.0 / p);
     }
-    P[i] = out;
+    if (lane == 0) P[i] = out;
   }
 }
 
@@ -254,6 +289,10 @@ struct mprof_ctx {
   int2* tiles_d = nullptr;
   size_t tiles_cap = 0;
   long long tiles_key[6] = {-1, -1, -1, -1, -1, -1};
+  // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
+  const double* stats_t = nullptr;
+  uint64_t stats_n = 0, stats_m = 0;
+  double stats_thr = -1.0;
 };
 
 namespace {
@@ -314,6 +353,21 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   w->mu = reinterpret_cast<double*>(base + nA + nB);
   w->best = reinterpret_cast<BestEntry*>(base + nA + 2 * nB);
   w->cmin = reinterpret_cast<int*>(base + nA + 2 * nB + nBest);
+  return MPROF_OK;
+}
+
+int32_t ensure_znorm_stats(mprof_ctx* c, const double* d_t, uint64_t n, const mprof_config* cfg,
+                           const Workspace& w) {
+  if (c->stats_t == d_t && c->stats_n == n && c->stats_m == cfg->m &&
+      c->stats_thr == cfg->flat_threshold)
+    return MPROF_OK;
+  const int L = (int)(n - cfg->m + 1);
+  k_znorm_stats<<<grid_for(L), 256, 0, c->stream>>>(d_t, L, (int)cfg->m, cfg->flat_threshold, w.mu, w.B);
+  CK(cudaGetLastError());
+  c->stats_t = d_t;
+  c->stats_n = n;
+  c->stats_m = cfg->m;
+  c->stats_thr = cfg->flat_threshold;
   return MPROF_OK;
 }
 
@@ -458,7 +512,9 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   ++launches;
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
   if (zn) {
-    k_znorm_stats<<<g, 256, 0, c->stream>>>(d_t, L, m, cfg->flat_threshold, w.mu, w.B);
+    c->stats_t = nullptr;  // force: the series bytes behind d_t may have changed
+    st = ensure_znorm_stats(c, d_t, n64, cfg, w);
+    if (st != MPROF_OK) return st;
     k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
     launches += 2;
   } else {
@@ -539,7 +595,7 @@ int32_t host_entry(mprof_ctx* in, const double* t, uint64_t n, const mprof_confi
   CK(cudaMemcpyAsync(d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   st = sweep_impl(c, d_t, n, cfg, 0, 0, d_cmp, d_idx, info);
   if (st != MPROF_OK) return st;
-  st = mprof_finalize_device(c, d_cmp, L, cfg, d_P);
+  st = mprof_finalize_device(c, d_t, n, d_cmp, d_idx, cfg, d_P);
   if (st != MPROF_OK) return st;
   if (info) info->kernel_launches += 1;
   CK(cudaMemcpyAsync(P, d_P, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -692,14 +748,25 @@ int32_t mprof_sweep_device(mprof_ctx* in, const double* d_t, uint64_t n, const m
   return sweep_impl(c, d_t, n, cfg, k_lo, k_hi, d_cmp, d_idx, info);
 }
 
-int32_t mprof_finalize_device(mprof_ctx* in, const double* d_cmp, uint64_t L, const mprof_config* cfg,
-                              double* d_P) {
-  if (!d_cmp || !cfg || !d_P) return fail(MPROF_E_BAD_ARG, "null argument");
-  mprof_ctx* c = nullptr;
-  int32_t st = resolve_ctx(in, &c);
+int32_t mprof_finalize_device(mprof_ctx* in, const double* d_t, uint64_t n, const double* d_cmp,
+                              const int64_t* d_idx, const mprof_config* cfg, double* d_P) {
+  if (!d_t || !d_cmp || !d_idx || !cfg || !d_P) return fail(MPROF_E_BAD_ARG, "null argument");
+  int32_t st = check_config(n, cfg);
   if (st != MPROF_OK) return st;
-  k_finalize<<<grid_for((long long)L), 256, 0, c->stream>>>(d_cmp, d_P, (int)L, cfg->family, cfg->p,
-                                                           (double)cfg->m);
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  const int L = (int)(n - cfg->m + 1);
+  Workspace w;
+  st = carve(c, L, &w);
+  if (st != MPROF_OK) return st;
+  if (cfg->family == MPROF_ZNORMALIZED) {
+    st = ensure_znorm_stats(c, d_t, n, cfg, w);
+    if (st != MPROF_OK) return st;
+  }
+  k_finalize<<<grid_for(32LL * L), 256, 0, c->stream>>>(d_t, d_cmp, d_idx, w.mu, w.B, d_P, L,
+                                                          (int)cfg->m, cfg->family, cfg->p,
+                                                          cfg->exact ? 1 : 0);
   CK(cudaGetLastError());
   return MPROF_OK;
 }

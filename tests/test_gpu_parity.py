@@ -1,0 +1,323 @@
+"""Parity tests proper: the CUDA path (through the C ABI) against the reference's golden vectors
+and the pinned CPU oracle, with the rules of SURVEY.md §8(d) (oracle/parity.py):
+
+* FP64: P within 1e-9 relative (`within`, tests/helpers.hpp:27-31) of the reference, or closer to
+  the long-double exact distance than the reference is (reference drift); I identical except
+  for ties within that tolerance.
+* z-normalized near-duplicates (rule 3b): |P - d*| <= ZN_ABS and ties under ZN_ABS.
+* exact (parity build) mode: comparison values and I BIT-identical to the reference run with the
+  same refresh_interval (AAMP, p = 1, 3, 4).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import EUCLIDEAN, PNORM, ZNORM
+from oracle.parity import check, within
+from paper_1901_05708_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+ZN_ABS = 2e-6   # rule 3b bound for z-normalized near-duplicates (measured: see DESIGN.md)
+FAM = {EUCLIDEAN: "euclidean", PNORM: "pnorm", ZNORM: "znorm"}
+
+
+def kind_of(mp, fam, p):
+    return {EUCLIDEAN: mp.DistanceKind.euclidean(), PNORM: mp.DistanceKind.pnorm(p),
+            ZNORM: mp.DistanceKind.znormalized()}[fam]
+
+
+def gpu(mp, t, m, fam=EUCLIDEAN, p=2.0, exclusion=1, refresh=0, exact=False, flat=None,
+        variant=None):
+    ts = mp.make_time_series(t)
+    cfg = mp.ProfileConfig(m, kind_of(mp, fam, p))
+    cfg.exclusion = exclusion
+    cfg.refresh_interval = refresh
+    cfg.exact = exact
+    if flat is not None:
+        cfg.flat_threshold = flat
+    if fam == EUCLIDEAN:
+        r = mp.aamp(ts, cfg)
+    elif fam == PNORM:
+        r = mp.aamp_pnorm(ts, cfg)
+    else:
+        r = mp.acamp(ts, cfg, mp.AcampVariant.FScore if variant is None else variant)
+    return r.distances, r.nn_index
+
+
+def assert_parity(t, m, fam, p, Pg, Ig, Pr, Ir, tol=TOL, exclusion=1):
+    rep = check(t, m, fam, Pg, Ig, Pr, Ir, tol=tol, p=p, abs_bound=ZN_ABS if fam == ZNORM else None)
+    assert rep.ok, rep.summary()
+    # admissibility of every reported neighbour
+    ok = Ig >= 0
+    assert np.all(np.abs(Ig[ok] - np.arange(Ig.size)[ok]) >= exclusion)
+    return rep
+
+
+# ---- known answers (the reference's own unit tests) --------------------------------------------
+
+ZIG = [0, 1, 2, 1, 0, 1, 2]
+
+
+def test_zigzag_all_families(mp):
+    P, I = gpu(mp, ZIG, 3)  # tests/test_aamp.cpp:63-72
+    assert np.all(within(P, [0, math.sqrt(3)] * 1 + [math.sqrt(3)] * 2 + [0], 1e-12))
+    assert list(I) == [4, 0, 1, 0, 0]
+    P, I = gpu(mp, ZIG, 3, PNORM, 3.0)  # tests/acceptance.cpp:193-201
+    assert np.all(within(P, [0, 3 ** (1 / 3), 3 ** (1 / 3), 3 ** (1 / 3), 0], 1e-9))
+    for variant in (mp.AcampVariant.FScore, mp.AcampVariant.SquaredDistance):
+        P, I = gpu(mp, ZIG, 3, ZNORM, variant=variant)  # tests/test_acamp.cpp:181-191
+        assert np.all(within(P, [0, math.sqrt(6), math.sqrt(6), math.sqrt(6), 0], 1e-12))
+        assert I[0] == 4 and I[4] == 0
+
+
+def test_ties_smallest_index(mp):
+    P, I = gpu(mp, [0, 0, 0, 1], 2)  # tests/test_aamp.cpp:74-83
+    assert P[0] == 0.0 and P[1] == 0.0 and within(P[2], 1.0, 1e-15)
+    assert list(I) == [1, 0, 0]
+
+
+def test_flat_convention(mp):
+    # tests/test_acamp.cpp:205-220, acceptance.cpp:346-360
+    for variant in (mp.AcampVariant.FScore, mp.AcampVariant.SquaredDistance):
+        P, I = gpu(mp, [5, 5, 5, 1, 2], 2, ZNORM, variant=variant)
+        assert np.all(within(P, [0, 0, 2, 2], 1e-12)) and np.all(np.isfinite(P))
+        assert I[1] == 0
+    # tests/test_acamp.cpp:222-237, acceptance.cpp:362-377
+    r = np.random.default_rng(604)
+    s = r.uniform(-1, 1, 160)
+    s[40:70] = 7.0
+    s[120:135] = -3.0
+    Pb, Ib = oracle.brute(s, 8, ZNORM)
+    P, I = gpu(mp, s, 8, ZNORM)
+    assert np.all(within(P, Pb, 1e-6)) and np.all(np.isfinite(P))
+    flat = np.array([np.var(s[i:i + 8]) <= 8e-12 for i in range(P.size)])
+    fl = np.flatnonzero(flat)
+    assert np.all(P[flat] == 0.0)
+    for i in fl:  # smallest other flat window (exclusion 1)
+        assert I[i] == next(f for f in fl if f != i)
+
+
+def test_no_admissible_pair(mp):
+    r = np.random.default_rng(511)  # tests/test_aamp.cpp:213-228
+    t = r.uniform(-1, 1, 24)
+    for fam, p in [(EUCLIDEAN, 2.0), (PNORM, 3.0), (ZNORM, 2.0)]:
+        P, I = gpu(mp, t, 4, fam, p, exclusion=16)
+        Pb, Ib = oracle.brute(t, 4, fam, p, exclusion=16)
+        assert np.array_equal(np.isinf(P), np.isinf(Pb)) and np.array_equal(I < 0, Ib < 0)
+        assert np.isinf(P[10]) and I[10] == -1
+        fin = np.isfinite(P)
+        assert np.all(within(P[fin], Pb[fin], 1e-9))
+
+
+def test_refresh_offset_series(mp):
+    r = np.random.default_rng(505)  # tests/test_aamp.cpp:174-187
+    t = r.uniform(-1, 1, 600) + 1e8
+    for exact in (False, True):
+        P, _ = gpu(mp, t, 16, refresh=32, exact=exact)
+        Pb, _ = oracle.brute(t, 16)
+        assert np.all(within(P, Pb, 1e-9))
+
+
+@pytest.mark.parametrize("n,m,excl", [(2, 1, 1), (3, 1, 1), (3, 2, 1), (5, 1, 4), (10, 3, 7),
+                                      (40, 39, 1), (1100, 5, 1), (1100, 5, 1094), (2500, 30, 1),
+                                      (2049, 1, 1), (3000, 64, 1025)])
+def test_edge_shapes_match_brute(mp, n, m, excl):
+    r = np.random.default_rng(n * 7 + m)
+    t = np.cumsum(r.standard_normal(n))
+    for fam, p in [(EUCLIDEAN, 2.0), (PNORM, 1.0), (PNORM, 3.0), (PNORM, 2.5), (ZNORM, 2.0)]:
+        if n > 1500 and fam == PNORM and p == 2.5:
+            continue
+        P, I = gpu(mp, t, m, fam, p, exclusion=excl)
+        if n <= 1200:
+            Pr, Ir = oracle.brute(t, m, fam, p, exclusion=excl)
+        else:
+            _, Pr, Ir = oracle.scan(t, m, fam, p, exclusion=excl)
+        assert_parity(t, m, fam, p, P, I, Pr, Ir, exclusion=excl)
+
+
+# ---- committed reference outputs ----------------------------------------------------------------
+
+def test_reference_fixtures(mp, golden):
+    g = golden["fixtures"]
+    for name, fam, p in [("euclidean", EUCLIDEAN, 2.0), ("pnorm", PNORM, 3.0), ("znorm", ZNORM, 2.0)]:
+        t = g[f"{name}_t"]
+        P, I = gpu(mp, t, 50, fam, p)
+        assert_parity(t, 50, fam, p, P, I, g[f"{name}_P"], g[f"{name}_I"])
+        # CLI acceptance tolerance against the brute-force oracle (acceptance.cpp:410)
+        assert np.all(within(P, g[f"{name}_Pbrute"], 1e-6))
+        if fam == ZNORM:
+            assert_parity(t, 50, fam, p, P, I, g[f"{name}_Psq"], g[f"{name}_Isq"])
+
+
+def test_reference_corpus(mp, golden):
+    g = golden["corpus"]
+    for c in range(int(g["count"])):
+        t, m = g[f"t{c}"], int(g[f"m{c}"])
+        P, I = gpu(mp, t, m)
+        assert_parity(t, m, EUCLIDEAN, 2.0, P, I, g[f"e_P{c}"], g[f"e_I{c}"])
+        for p in (1.0, 2.0, 3.0, 4.5):
+            P, I = gpu(mp, t, m, PNORM, p)
+            assert_parity(t, m, PNORM, p, P, I, g[f"p{p}_P{c}"], g[f"p{p}_I{c}"])
+        for tag, variant in (("zf", mp.AcampVariant.FScore), ("zs", mp.AcampVariant.SquaredDistance)):
+            P, I = gpu(mp, t, m, ZNORM, variant=variant)
+            assert_parity(t, m, ZNORM, 2.0, P, I, g[f"{tag}_P{c}"], g[f"{tag}_I{c}"])
+
+
+def _sweep_cmp(mp, t, m, fam, p, exclusion, refresh, exact, k_lo=0, k_hi=0, ctx=None):
+    torch = pytest.importorskip("torch")
+    d_t = torch.tensor(t, dtype=torch.float64, device="cuda")
+    L = t.size - m + 1
+    cmp = torch.empty(L, dtype=torch.float64, device="cuda")
+    idx = torch.empty(L, dtype=torch.int64, device="cuda")
+    cfg = mp.ProfileConfig(m, kind_of(mp, fam, p))
+    cfg.exclusion, cfg.refresh_interval, cfg.exact = exclusion, refresh, exact
+    torch.cuda.synchronize()  # the library runs on its own stream
+    mp.sweep_device(d_t.data_ptr(), t.size, cfg, k_lo, k_hi, cmp.data_ptr(), idx.data_ptr(), ctx=ctx)
+    torch.cuda.synchronize()
+    return cmp.cpu().numpy(), idx.cpu().numpy()
+
+
+def test_exact_mode_bit_identical_to_reference(mp, golden):
+    """Parity build: no FMA, clamp propagated, runs seeded at multiples of refresh_interval ->
+    the comparison values equal the reference's bit for bit (SURVEY.md §7 hard part 5)."""
+    g = golden["exact"]
+    for name in ("walk", "walk_excl", "walk_r1", "walk_r7"):
+        t = g[f"{name}_t"]
+        m, R, excl = (int(x) for x in g[f"{name}_meta"])
+        for tag, fam, p in [("e", EUCLIDEAN, 2.0), ("p1", PNORM, 1.0), ("p3", PNORM, 3.0), ("p4", PNORM, 4.0)]:
+            cmp, idx = _sweep_cmp(mp, t, m, fam, p, excl, R, True)
+            assert np.array_equal(cmp, g[f"{name}_{tag}_cmp"]), (name, tag, int(np.sum(cmp != g[f"{name}_{tag}_cmp"])))
+            assert np.array_equal(idx, g[f"{name}_{tag}_I"]), (name, tag)
+            P, I = gpu(mp, t, m, fam, p, exclusion=excl, refresh=R, exact=True)
+            Pr = g[f"{name}_{tag}_P"]
+            if fam == EUCLIDEAN or p == 1.0:
+                assert np.array_equal(P, Pr)  # sqrt / identity are correctly rounded
+            else:
+                assert np.all(within(P, Pr, 4e-16))  # CUDA pow vs glibc pow
+            assert np.array_equal(I, g[f"{name}_{tag}_I"])
+
+
+def test_exact_mode_whole_diagonal_runs(mp):
+    """refresh_interval = 0 in exact mode: one chained run per diagonal, like the reference."""
+    r = np.random.default_rng(9)
+    t = 1000 + np.cumsum(r.standard_normal(1500))
+    for fam, p in [(EUCLIDEAN, 2.0), (PNORM, 1.0), (PNORM, 3.0)]:
+        cmp, idx = _sweep_cmp(mp, t, 40, fam, p, 1, 0, True)
+        c_or, _, I_or = oracle.scan(t, 40, fam, p)
+        assert np.array_equal(cmp, c_or) and np.array_equal(idx, I_or)
+
+
+# ---- seeded workloads vs the oracle ----------------------------------------------------------------
+
+@pytest.mark.parametrize("excl_kind", ["1", "m", "quarter"])
+def test_c1_aamp(mp, excl_kind):
+    t = W.c1()
+    m = 100
+    excl = {"1": 1, "m": m, "quarter": (t.size - m) // 4}[excl_kind]
+    P, I = gpu(mp, t, m, exclusion=excl)
+    _, Pr, Ir = oracle.scan(t, m, exclusion=excl)
+    assert_parity(t, m, EUCLIDEAN, 2.0, P, I, Pr, Ir, exclusion=excl)
+
+
+@pytest.mark.parametrize("excl_kind", ["1", "m"])
+def test_c2_acamp_prefix(mp, excl_kind):
+    t = W.c2(n=32768, motifs=6, flats=3)
+    m = 256
+    excl = {"1": 1, "m": m}[excl_kind]
+    P, I = gpu(mp, t, m, ZNORM, exclusion=excl)
+    _, Pr, Ir = oracle.scan(t, m, ZNORM, exclusion=excl)
+    assert_parity(t, m, ZNORM, 2.0, P, I, Pr, Ir, exclusion=excl)
+
+
+@pytest.mark.parametrize("p", [1.0, 3.0])
+def test_c3_pnorm_prefix(mp, p):
+    t = W.c3(n=24576)
+    m = 128
+    P, I = gpu(mp, t, m, PNORM, p)
+    _, Pr, Ir = oracle.scan(t, m, PNORM, p)
+    rep = assert_parity(t, m, PNORM, p, P, I, Pr, Ir)
+    # far neighbours: this workload exercises diagonals k >> 1 at exclusion 1
+    assert np.median(np.abs(I - np.arange(I.size))) > 50, rep.summary()
+
+
+def test_c2_full_flat_and_motifs(mp):
+    """Full C2: every fully flat window has P = 0 and I = smallest other flat window; planted
+    exact affine motif copies get P ~ 0 (the reference reports up to 3e-4 there)."""
+    t = W.c2()
+    m = 256
+    P, I = gpu(mp, t, m, ZNORM)
+    L = P.size
+    v = np.lib.stride_tricks.sliding_window_view(t, m)
+    var = v.var(axis=1)
+    flat = np.flatnonzero(var <= 1e-12 * m)
+    assert flat.size >= 5 * 200
+    assert np.all(P[flat] == 0.0)
+    for i in flat[:: max(1, flat.size // 50)]:
+        assert I[i] == (flat[0] if flat[0] != i else flat[1])
+    # motif starts: windows equal to level + burst (detect via the generator's structure)
+    assert np.sum(P < 1e-6) >= flat.size + 20
+    assert np.all(np.isfinite(P)) and np.all(P <= 2 * math.sqrt(m) + 1e-9)
+    # sampled exact neighbours
+    rows = np.random.default_rng(0).choice(L, 6, replace=False)
+    best, arg = oracle.exact_rows(t, m, rows, ZNORM)
+    assert np.all(np.abs(P[rows] - best) <= ZN_ABS)
+
+
+def test_c3_full_holder_sandwich(mp):
+    """Full C3: L^p norms are non-increasing in p and Hölder bounds them: P3 <= P1 <= m^(2/3) P3."""
+    t = W.c3()
+    m = 128
+    P1, _ = gpu(mp, t, m, PNORM, 1.0)
+    P3, _ = gpu(mp, t, m, PNORM, 3.0)
+    assert np.all(P3 <= P1 * (1 + 1e-12))
+    assert np.all(P1 <= m ** (2 / 3) * P3 * (1 + 1e-12))
+
+
+# ---- bands and merge --------------------------------------------------------------------------------
+
+def test_bands_merge_to_full_profile(mp):
+    torch = pytest.importorskip("torch")
+    r = np.random.default_rng(21)
+    t = 50 + np.cumsum(r.standard_normal(9000))
+    m, R = 64, 512
+    for fam, p in [(EUCLIDEAN, 2.0), (PNORM, 3.0)]:
+        full_c, full_i = _sweep_cmp(mp, t, m, fam, p, 1, R, True)
+        cuts = mp.band_cuts(t.size, m, 1, 3)
+        dev = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            c, i = _sweep_cmp(mp, t, m, fam, p, 1, R, True, a, b)
+            dev.append((torch.tensor(c, device="cuda"), torch.tensor(i, device="cuda")))
+        c0, i0 = dev[0]
+        torch.cuda.synchronize()
+        for c1, i1 in dev[1:]:
+            mp.merge_device(c0.data_ptr(), i0.data_ptr(), c1.data_ptr(), i1.data_ptr(), c0.numel())
+        torch.cuda.synchronize()
+        assert np.array_equal(c0.cpu().numpy(), full_c) and np.array_equal(i0.cpu().numpy(), full_i)
+    # fast mode, z-norm: bands + merge within tolerance of the oracle
+    cuts = mp.band_cuts(t.size, m, 1, 4)
+    L = t.size - m + 1
+    cm = np.full(L, np.inf)
+    im = np.full(L, -1)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        c, i = _sweep_cmp(mp, t, m, ZNORM, 2.0, 1, 0, False, a, b)
+        better = (c < cm) | ((c == cm) & (i < im))
+        cm, im = np.where(better, c, cm), np.where(better, i, im)
+    _, Pr, Ir = oracle.scan(t, m, ZNORM)
+    d_t = torch.tensor(t, device="cuda")
+    P = torch.empty(L, dtype=torch.float64, device="cuda")
+    cfg = mp.ProfileConfig(m, mp.DistanceKind.znormalized())
+    d_cm = torch.tensor(cm, device="cuda")
+    d_im = torch.tensor(im, device="cuda")
+    torch.cuda.synchronize()
+    mp.finalize_device(d_t.data_ptr(), t.size, d_cm.data_ptr(), d_im.data_ptr(), cfg, P.data_ptr())
+    torch.cuda.synchronize()
+    assert_parity(t, m, ZNORM, 2.0, P.cpu().numpy(), im, Pr, Ir)
+
+
+def test_fp64_peak_is_plausible(mp):
+    g, ms = mp.fp64_peak()
+    assert 5e3 < g < 1e5, g  # GFLOP/s
