@@ -34,6 +34,9 @@ __all__ = [
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libmprof_gpu.so"
+# experiments only: load a tile-parameter variant built by tools/build_variants.py
+if __import__("os").environ.get("MPROF_GPU_LIB"):
+    LIB_PATH = Path(__import__("os").environ["MPROF_GPU_LIB"])
 
 
 class ErrorCode(enum.IntEnum):

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -26,9 +27,21 @@ using namespace mpg;
 namespace {
 
 // ---- tile configuration (one instantiation for every family) -------------------------------
-constexpr int kD = 8;    // diagonals per thread
-constexpr int kT = 128;  // threads per CTA
-constexpr int kS = 64;   // rows per shared-memory stage
+#ifndef MPROF_TILE_D
+#define MPROF_TILE_D 8
+#endif
+#ifndef MPROF_TILE_T
+#define MPROF_TILE_T 128
+#endif
+#ifndef MPROF_TILE_S
+#define MPROF_TILE_S 128
+#endif
+#ifndef MPROF_MIN_BLOCKS
+#define MPROF_MIN_BLOCKS 4
+#endif
+constexpr int kD = MPROF_TILE_D;  // diagonals per thread
+constexpr int kT = MPROF_TILE_T;  // threads per CTA
+constexpr int kS = MPROF_TILE_S;  // rows per shared-memory stage
 constexpr int kK = kD * kT;
 
 thread_local std::string g_last_error;
@@ -417,9 +430,9 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, long long R, long l
 template <class P>
 int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int k1,
                      bool first_diag, uint32_t* launches, float* ms) {
-  using SB = StageBuf<P::kHasB, kD, kT, kS>;
-  const size_t smem = 2 * sizeof(SB);
-  auto kern = sweep_kernel<P, kD, kT, kS>;
+  using SM = SweepSmem<P::kHasB, kD, kT, kS>;
+  const size_t smem = sizeof(SM);
+  auto kern = sweep_kernel<P, kD, kT, kS, MPROF_MIN_BLOCKS>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (first_diag && k1 <= prm.L - 1) {
     k_first_diag<P><<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);
@@ -542,8 +555,22 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     prm.k_hi = (int)k_hi;
     prm.R = (int)std::min<long long>(R, INT_MAX);
     prm.p = cfg->p;
+    prm.stats = nullptr;
+    const bool want_stats = getenv("MPROF_STATS") != nullptr;
+    if (want_stats) {
+      CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
+      CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
+    }
     st = dispatch_sweep(c, cfg, prm, ntiles, (int)k_lo, &launches, &ms);
     if (st != MPROF_OK) return st;
+    if (want_stats) {
+      unsigned long long h[2];
+      CK(cudaMemcpyAsync(h, prm.stats, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFreeAsync(prm.stats, c->stream);
+      fprintf(stderr, "[mprof stats] family %d L %d tiles %lld R %lld: replays %llu offers %llu\n",
+              cfg->family, L, ntiles, R, h[0], h[1]);
+    }
     if (zn) {
       const int nch = (L + kChunk - 1) / kChunk;
       k_flat_chunk_min<<<nch, 256, 0, c->stream>>>(w.B, L, w.cmin);

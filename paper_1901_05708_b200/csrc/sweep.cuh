@@ -180,21 +180,32 @@ struct Znorm {
 
 template <int D, int T, int S>
 struct Geo {
-  static constexpr int K = T * D;      // diagonals per tile
-  static constexpr int NCOL = S + K;   // column slots touched by one stage
+  static constexpr int K = T * D;        // diagonals per tile
+  static constexpr int NCOL = S + K;     // column operands live during one stage
+  static constexpr int RING = K + 2 * S; // ring slots: live stage + the prefetched next stage
   __host__ __device__ static constexpr int pad(int x) { return x + x / D; }
   static constexpr int NCOLP = pad(NCOL - 1) + 1;
+  static constexpr int RINGP = pad(RING - 1) + 1;
 };
 
+// Shared memory of one CTA. Column operands live in a RING indexed by X = (column position -
+// tile column base): stage st uses X in [st*S, st*S + S + K) and prefetches only its S new
+// operands for stage st+1, so one copy of the K-wide window is resident (not two). Thresholds
+// (4 B per column) are re-read for the whole live window every stage (fresh minima from other
+// CTAs) and double-buffered with the row operands.
 template <bool HASB, int D, int T, int S>
-struct StageBuf {
+struct SweepSmem {
   using G = Geo<D, T, S>;
-  double2 colA[G::NCOLP];               // A[i0 + kb + x]
-  double colB[HASB ? G::NCOLP : 2];     // B[i0 + kb + 1 + x]
-  int colT[G::NCOLP];                   // hi32(best[i0 + kb + 1 + x].v)
-  double2 rowA[S];                      // A[i0 + x]
-  double rowB[HASB ? S : 2];            // B[i0 + 1 + x]
-  int rowT[S];                          // hi32(best[i0 + 1 + x].v)
+  static_assert(G::RING % D == 0 && S % D == 0, "stage and ring must be multiples of D");
+  static constexpr int NCB = G::NCOL / D + 1;  // column blocks of D
+  double2 colA[G::RINGP];                      // ring: A[cbase + X] at pad(X mod RING)
+  double colB[HASB ? G::RINGP : 2];            // ring: B[cbase + 1 + X]
+  int colT[2][G::NCOLP];                       // hi32(best[i0 + kb + 1 + x].v), exact
+  int colBM[2][NCB];                           // max of colT over aligned blocks of D
+  double2 rowA[2][S];                          // A[i0 + x]
+  double rowB[2][HASB ? S : 2];                // B[i0 + 1 + x]
+  int rowT[2][S];                              // hi32(best[i0 + 1 + x].v), exact
+  int rowBM[2][S / D];                         // max of rowT over aligned blocks of D
 };
 
 struct SweepParams {
@@ -208,6 +219,7 @@ struct SweepParams {
   int k_hi;               // exclusive upper bound of the swept diagonal band
   int R;                  // rows per tile
   double p;
+  unsigned long long* stats;  // optional diagnostics (MPROF_STATS): [0] replays [1] offers
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -241,152 +253,226 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int D>
 struct Cells {
   double v[D];
-  int tc[D];
 };
 
-template <int D, bool FORCE>
-__device__ __noinline__ Cells<D> resolve(Cells<D> c, unsigned valid, int row, int tr, int col0,
-                                         BestEntry* best, int* rowT, int* colT, int colx0) {
+// Exact slow path for one BLOCK of D sub-steps of ONE lane, called divergently when the block's
+// minimum high word passed the block threshold. The block is REPLAYED from the accumulators saved
+// at its start with the identical arithmetic (bit-identical cell values), and every cell whose
+// high word is <= the current exact column (row) threshold in shared memory (colT / rowT) is
+// merged into the global column (row) minimum; thresholds are lowered with shared atomicMin.
+template <class P, int D>
+struct Acc {
+  double a[D];
+};
+
+template <class P, int D, int RING>
+__device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0, int xb, int kt,
+                                          int kend, int L, double p, int X0, const double2* colA,
+                                          const double* colB, int* colT, const double2* rowA,
+                                          const double* rowB, int* rowT, BestEntry* best,
+                                          unsigned long long* stats) {
+  using G = Geo<D, 1, 1>;
+  if (stats) atomicAdd(&stats[0], 1ull);
+  for (int u = 0; u < D && s + u < cnt; ++u) {
+    const int x = s + u;
+    const double2 r = rowA[x];
+    const double rb = P::kHasB ? rowB[x] : 0.0;
+    const int row = i0 + x + 1;
+    const int tr = *reinterpret_cast<volatile int*>(&rowT[x]);
+    unsigned long long rv = kInfBits;
+    int rj = INT_MAX;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int q = G::pad((X0 + x + xb + d) % RING);
+      acc.a[d] = P::step(acc.a[d], r, colA[q], p);
+      const double v = P::score(acc.a[d], rb, P::kHasB ? colB[q] : 0.0);
+      if (!((kt + d < kend) && (row + kt + d <= L - 1))) continue;
+      const int h = __double2hiint(v);
+      int* ct = &colT[G::pad(x + xb + d)];
+      const bool rowhit = h <= tr;
+      const bool colhit = h <= *reinterpret_cast<volatile int*>(ct);
+      if (!(rowhit || colhit)) continue;
+      // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
+      const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+      const int j = row + kt + d;
+      if (colhit) {
+        atomicMin(ct, static_cast<int>(offer(best, j, vb, row) >> 32));
+        if (stats) atomicAdd(&stats[1], 1ull);
+      }
+      if (rowhit && lex_less(vb, j, rv, rj)) {
+        rv = vb;
+        rj = j;
+      }
+    }
+    if (rj != INT_MAX) {
+      atomicMin(&rowT[x], static_cast<int>(offer(best, row, rv, rj) >> 32));
+      if (stats) atomicAdd(&stats[1], 1ull);
+    }
+  }
+}
+
+// Merge of the seed cells (every valid cell, all lanes on the same row): columns per cell, the
+// row through a warp lexicographic reduction and one CAS per warp. Called convergently.
+template <int D>
+__device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, int col0,
+                                          BestEntry* best) {
   unsigned long long rv = kInfBits;
   int rj = INT_MAX;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     if (!((valid >> d) & 1u)) continue;
     const double v = c.v[d];
-    const int h = __double2hiint(v);
-    const bool rowhit = FORCE || h <= tr;
-    const bool colhit = FORCE || h <= c.tc[d];
-    if (!(rowhit || colhit)) continue;
-    // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
-    const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned long long vb = (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
     const int j = col0 + d;
-    if (colhit) {
-      const unsigned long long nb = offer(best, j, vb, row);
-      const int nh = static_cast<int>(nb >> 32);
-      c.tc[d] = min(c.tc[d], nh);
-      if (colT) atomicMin(&colT[Geo<D, 1, 1>::pad(colx0 + d)], nh);
-    }
-    if (rowhit && lex_less(vb, j, rv, rj)) {
+    offer(best, j, vb, row);
+    if (lex_less(vb, j, rv, rj)) {
       rv = vb;
       rj = j;
     }
   }
-  if (__any_sync(0xffffffffu, rj != INT_MAX)) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const unsigned long long ov = __shfl_xor_sync(0xffffffffu, rv, off);
-      const int oj = __shfl_xor_sync(0xffffffffu, rj, off);
-      if (lex_less(ov, oj, rv, rj)) {
-        rv = ov;
-        rj = oj;
-      }
-    }
-    if ((threadIdx.x & 31) == 0 && rj != INT_MAX) {
-      const unsigned long long nb = offer(best, row, rv, rj);
-      if (rowT) atomicMin(rowT, static_cast<int>(nb >> 32));
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long ov = __shfl_xor_sync(0xffffffffu, rv, off);
+    const int oj = __shfl_xor_sync(0xffffffffu, rj, off);
+    if (lex_less(ov, oj, rv, rj)) {
+      rv = ov;
+      rj = oj;
     }
   }
-  return c;
+  if ((threadIdx.x & 31) == 0 && rj != INT_MAX) offer(best, row, rv, rj);
 }
 
 // ---------------------------------------------------------------------------------------------
 // One stage of S (or cnt < S) row transitions i -> i+1, i in [i0, i0+cnt).
+// Filter: per block of D sub-steps a thread touches D rows and 2D-1 columns; theta = max of
+// their thresholds (three shared loads per block, precomputed block maxima). A cell can only
+// improve (or tie) its row or column minimum if its high word is <= theta. The hot loop only
+// keeps the running minimum high word of the block (a VIMNMX3 tree, no branch); a block that
+// passes is replayed exactly by `replay_block`.
 
 template <class P, int D, int T, int S, bool GUARD>
-__device__ __forceinline__ void run_stage(StageBuf<P::kHasB, D, T, S>& sb, double (&acc)[D],
-                                          int i0, int cnt, int kt, int kend, int L,
-                                          BestEntry* best, double p) {
+__device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int b, int X0,
+                                          double (&acc)[D], int i0, int cnt, int kt, int kend,
+                                          int L, BestEntry* best, double p,
+                                          unsigned long long* stats) {
   using G = Geo<D, T, S>;
   const int xb = threadIdx.x * D;
   double2 cA[D];
   double cB[D];
-  int tc[D];
+  {
+    const int q0 = G::pad((X0 + xb) % G::RING);  // X0 + xb is a multiple of D: no wrap inside
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    cA[d] = sb.colA[G::pad(xb + d)];
-    if constexpr (P::kHasB) cB[d] = sb.colB[G::pad(xb + d)];
-    tc[d] = sb.colT[G::pad(xb + d)];
+    for (int d = 0; d < D; ++d) {
+      cA[d] = sm.colA[q0 + d];
+      if constexpr (P::kHasB) cB[d] = sm.colB[q0 + d];
+    }
   }
+  const double2* rowA = sm.rowA[b];
+  const double* rowB = sm.rowB[b];
   for (int s = 0; s < cnt; s += D) {
-    // pad(s + xb + D + u) == qn + u for u < D (s + xb + D is a multiple of D): constant offsets
-    const int qn = G::pad(s + xb + D);
-    const double2* nA = &sb.colA[qn];
-    const double* nB = &sb.colB[P::kHasB ? qn : 0];
-    const int* nT = &sb.colT[qn];
+    // the D operands entering during this block are contiguous in the ring: constant offsets
+    const int qn = G::pad((X0 + s + xb + D) % G::RING);
+    const double2* nA = &sm.colA[qn];
+    const double* nB = &sm.colB[P::kHasB ? qn : 0];
+    const int cb = s / D + threadIdx.x;
+    const int theta = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
+    Acc<P, D> acc0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc0.a[d] = acc[d];
+    int hmin = INT_MAX;
 #pragma unroll
     for (int u = 0; u < D; ++u) {
       if (GUARD && s + u >= cnt) break;
       const int x = s + u;
-      const double2 r = sb.rowA[x];
+      const double2 r = rowA[x];
       double rb = 0.0;
-      if constexpr (P::kHasB) rb = sb.rowB[x];
-      const int tr = sb.rowT[x];
+      if constexpr (P::kHasB) rb = rowB[x];
       const int row = i0 + x + 1;
-      Cells<D> c;
-      bool hit = false;
-      unsigned valid = (1u << D) - 1u;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int sl = (d + u) % D;
         acc[d] = P::step(acc[d], r, cA[sl], p);
-        c.v[d] = P::score(acc[d], rb, P::kHasB ? cB[sl] : 0.0);
-        c.tc[d] = tc[sl];
-        const int h = __double2hiint(c.v[d]);
-        bool ok = true;
-        if (GUARD) {
-          ok = (kt + d < kend) && (row + kt + d <= L - 1);
-          if (!ok) valid &= ~(1u << d);
-        }
-        hit |= ok && ((h <= tr) || (h <= tc[sl]));
-      }
-      if (__any_sync(0xffffffffu, hit)) {
-        c = resolve<D, false>(c, valid, row, tr, row + kt, best, &sb.rowT[x], sb.colT, x + xb);
-#pragma unroll
-        for (int d = 0; d < D; ++d) tc[(d + u) % D] = c.tc[d];
+        const double v = P::score(acc[d], rb, P::kHasB ? cB[sl] : 0.0);
+        int h = __double2hiint(v);
+        if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
+        hmin = min(hmin, h);
       }
       // slide the column ring: slot u (used by d = 0 this substep) takes the next operand
       cA[u] = nA[u];
       if constexpr (P::kHasB) cB[u] = nB[u];
-      tc[u] = nT[u];
     }
+    if (hmin <= theta)
+      replay_block<P, D, G::RING>(acc0, s, cnt, i0, xb, kt, kend, L, p, X0, sm.colA, sm.colB,
+                                  sm.colT[b], sm.rowA[b], sm.rowB[b], sm.rowT[b], best, stats);
   }
 }
 
-// Issue the cp.async copies of one stage (rows i0 .. i0+S-1 transitions).
+// Block maxima of the freshly loaded thresholds (after the stage's cp.async completed).
 template <bool HASB, int D, int T, int S>
-__device__ __forceinline__ void load_stage(StageBuf<HASB, D, T, S>& sb, const SweepParams& prm,
-                                           int i0, int kb) {
+__device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, int b) {
+  using G = Geo<D, T, S>;
+  using SM = SweepSmem<HASB, D, T, S>;
+  for (int blk = threadIdx.x; blk < SM::NCB; blk += T) {
+    int mx = INT_MIN;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int x = blk * D + d;
+      if (x < G::NCOL) mx = max(mx, sm.colT[b][G::pad(x)]);
+    }
+    sm.colBM[b][blk] = mx;
+  }
+  for (int blk = threadIdx.x; blk < S / D; blk += T) {
+    int mx = INT_MIN;
+#pragma unroll
+    for (int d = 0; d < D; ++d) mx = max(mx, sm.rowT[b][blk * D + d]);
+    sm.rowBM[b][blk] = mx;
+  }
+}
+
+// Issue the cp.async copies of stage st (row transitions i0 .. i0+S-1, i0 = ra + st*S):
+// its row operands and thresholds, the thresholds of its whole live column window, and the
+// column operands that enter the ring with it (all NCOL for stage 0, S afterwards).
+template <bool HASB, int D, int T, int S>
+__device__ __forceinline__ void load_stage(SweepSmem<HASB, D, T, S>& sm, const SweepParams& prm,
+                                           int st, int ra, int kb) {
   using G = Geo<D, T, S>;
   const int L = prm.L;
+  const int b = st & 1;
+  const int i0 = ra + st * S;
   const int* bestw = reinterpret_cast<const int*>(prm.best);  // word view; hi word at +1
   for (int x = threadIdx.x; x < G::NCOL; x += T) {
-    const int pa = i0 + kb + x;       // A position
-    const int pb = pa + 1;            // B / threshold position (target column)
-    const bool va = pa < L - 1, vb = pb < L;
-    const int q = G::pad(x);
-    cp_async(&sb.colA[q], prm.A + (va ? pa : 0), va ? 16 : 0, 16);
-    if constexpr (HASB) cp_async(&sb.colB[q], prm.B + (vb ? pb : 0), vb ? 8 : 0, 8);
-    cp_async(&sb.colT[q], bestw + 4 * (vb ? pb : 0) + 1, vb ? 4 : 0, 4);
+    const int pb = i0 + kb + 1 + x;
+    const bool vb = pb < L;
+    cp_async(&sm.colT[b][G::pad(x)], bestw + 4 * (vb ? pb : 0) + 1, vb ? 4 : 0, 4);
+  }
+  const int Xlo = st == 0 ? 0 : st * S + G::K;
+  const int Xhi = st * S + G::NCOL;
+  for (int X = Xlo + threadIdx.x; X < Xhi; X += T) {
+    const int pa = ra + kb + X;
+    const bool va = pa < L - 1, vb = pa + 1 < L;
+    const int q = G::pad(X % G::RING);
+    cp_async(&sm.colA[q], prm.A + (va ? pa : 0), va ? 16 : 0, 16);
+    if constexpr (HASB) cp_async(&sm.colB[q], prm.B + (vb ? pa + 1 : 0), vb ? 8 : 0, 8);
   }
   for (int x = threadIdx.x; x < S; x += T) {
     const int pa = i0 + x;
     const int pb = pa + 1;
     const bool va = pa < L - 1, vb = pb < L;
-    cp_async(&sb.rowA[x], prm.A + (va ? pa : 0), va ? 16 : 0, 16);
-    if constexpr (HASB) cp_async(&sb.rowB[x], prm.B + (vb ? pb : 0), vb ? 8 : 0, 8);
-    cp_async(&sb.rowT[x], bestw + 4 * (vb ? pb : 0) + 1, vb ? 4 : 0, 4);
+    cp_async(&sm.rowA[b][x], prm.A + (va ? pa : 0), va ? 16 : 0, 16);
+    if constexpr (HASB) cp_async(&sm.rowB[b][x], prm.B + (vb ? pb : 0), vb ? 8 : 0, 8);
+    cp_async(&sm.rowT[b][x], bestw + 4 * (vb ? pb : 0) + 1, vb ? 4 : 0, 4);
   }
 }
 
 // ---------------------------------------------------------------------------------------------
 // The sweep kernel: one CTA per tile (kb, ra).
 
-template <class P, int D, int T, int S>
-__global__ void __launch_bounds__(T) sweep_kernel(const SweepParams prm) {
+template <class P, int D, int T, int S, int MINB>
+__global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   using G = Geo<D, T, S>;
-  using SB = StageBuf<P::kHasB, D, T, S>;
+  using SM = SweepSmem<P::kHasB, D, T, S>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SB* bufs = reinterpret_cast<SB*>(smem_raw);
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
   const int2 tl = prm.tiles[blockIdx.x];
   const int kb = tl.x, ra = tl.y;
@@ -412,8 +498,8 @@ __global__ void __launch_bounds__(T) sweep_kernel(const SweepParams prm) {
     // stage t[ra + l ...] (row) and t[ra + kb + l ...] (columns) through shared memory in
     // chunks of SL samples; summation order l = 0..m-1 as in direct_sq_acc.
     constexpr int SL = 2 * S;
-    static_assert(sizeof(SB) >= sizeof(double) * (SL + G::pad(G::K + SL)), "seed scratch");
-    double* srow = reinterpret_cast<double*>(bufs);
+    static_assert(sizeof(SM) >= sizeof(double) * (SL + G::pad(G::K + SL)), "seed scratch");
+    double* srow = reinterpret_cast<double*>(smem_raw);
     double* scol = srow + SL;
     const double mur = P::kCenteredSeed ? prm.mu[ra] : 0.0;
     const int xb = threadIdx.x * D;
@@ -456,33 +542,33 @@ __global__ void __launch_bounds__(T) sweep_kernel(const SweepParams prm) {
       const bool ok = (k < kend) && (ra + k <= L - 1);
       const double cb = (P::kHasB && ok) ? prm.B[ra + k] : 0.0;
       c.v[d] = P::score(acc[d], rb, cb);
-      c.tc[d] = 0;
       valid |= (ok ? 1u : 0u) << d;
     }
-    resolve<D, true>(c, valid, ra, 0, ra + kt, prm.best, nullptr, nullptr, 0);
+    resolve_seed<D>(c, valid, ra, ra + kt, prm.best);
   }
 
   // ---- stage pipeline over the row transitions ra .. re-2 ---------------------------------
   const int steps = re - 1 - ra;
   if (steps <= 0) return;
   __syncthreads();  // seed scratch reuse
-  load_stage<P::kHasB, D, T, S>(bufs[0], prm, ra, kb);
+  load_stage<P::kHasB, D, T, S>(sm, prm, 0, ra, kb);
   cp_async_commit();
-  int st = 0;
-  for (int s0 = 0; s0 < steps; s0 += S, ++st) {
+  for (int st = 0, s0 = 0; s0 < steps; s0 += S, ++st) {
     const int cnt = min(S, steps - s0);
     const int i0 = ra + s0;
-    if (s0 + S < steps) load_stage<P::kHasB, D, T, S>(bufs[(st + 1) & 1], prm, i0 + S, kb);
+    if (s0 + S < steps) load_stage<P::kHasB, D, T, S>(sm, prm, st + 1, ra, kb);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
+    stage_block_max<P::kHasB, D, T, S>(sm, st & 1);
+    __syncthreads();
     const bool full = (cnt == S) && (kb + G::K <= prm.k_hi) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {
-      run_stage<P, D, T, S, false>(bufs[st & 1], acc, i0, cnt, kt, kend, L, prm.best, prm.p);
+      run_stage<P, D, T, S, false>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     } else {
-      run_stage<P, D, T, S, true>(bufs[st & 1], acc, i0, cnt, kt, kend, L, prm.best, prm.p);
+      run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     }
-    __syncthreads();
+    __syncthreads();  // stage st's buffers (rows, thresholds, ring slots) are free for st+2
   }
 }
 
