@@ -71,15 +71,22 @@ int32_t cuda_fail(cudaError_t e, const char* what) {
 // ---------------------------------------------------------------------------------------------
 // auxiliary kernels
 
-__global__ void k_init_best(BestEntry* best, int L) {
+// Initial profile. With B (z-norm) flat windows are PINNED to (0, -1), an entry nothing can
+// beat and whose threshold word (0) no cell passes: every pair with a flat side scores exactly
+// d = 1 (or the flat-flat minimum), so flat rows/columns would otherwise tie on every cell of the
+// sweep. k_flat_fix assigns their final entries directly.
+__global__ void k_init_best(BestEntry* best, const double* __restrict__ B, int L) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
-    best[i] = BestEntry{kInfBits, kNoIdx};
+    best[i] = (B && B[i] == 0.0) ? BestEntry{0ull, -1} : BestEntry{kInfBits, kNoIdx};
 }
 
-// A[p] = (t[p], t[p+m]) for p in [0, L-1)
-__global__ void k_build_pairs(const double* __restrict__ t, double2* __restrict__ A, int L, int m) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L - 1; p += gridDim.x * blockDim.x)
-    A[p] = make_double2(t[p], t[p + m]);
+// A[p] for p in [0, L-1): kPairsRaw (t[p], t[p+m]); kPairsDeltaSum (t[p+m]-t[p], t[p+m]+t[p])
+__global__ void k_build_pairs(const double* __restrict__ t, double2* __restrict__ A, int L, int m,
+                              int kind) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L - 1; p += gridDim.x * blockDim.x) {
+    const double a = t[p], b = t[p + m];
+    A[p] = kind == kPairsDeltaSum ? make_double2(b - a, b + a) : make_double2(a, b);
+  }
 }
 
 // Per-window mean and inverse centred norm, two-pass (the well-conditioned form; the reference
@@ -170,15 +177,25 @@ __device__ int first_flat(const double* __restrict__ B, const int* __restrict__ 
   return INT_MAX;
 }
 
-// For every flat window i: partner = smallest flat f with |i - f| in the band [k_lo, k_hi)
-// (k_lo >= exclusion); if one exists the entry becomes (0, f).
+// Final entries of the flat windows i (pinned during the sweep), for the band of diagonals
+// [k_lo, k_hi) (k_lo >= exclusion): the smallest flat f with |i - f| in the band scores the
+// minimum (distance 0); without one, every admissible partner scores d = 1 (distance sqrt(2m))
+// and the smallest admissible index wins the tie; without any admissible partner: (+inf, -1).
 __global__ void k_flat_fix(const double* __restrict__ B, int L, int k_lo, int k_hi,
                            const int* __restrict__ cmin, BestEntry* best) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
     if (B[i] != 0.0) continue;
     int f = first_flat(B, cmin, max(0, i - k_hi + 1), i - k_lo);
     if (f == INT_MAX) f = first_flat(B, cmin, i + k_lo, min(L - 1, i + k_hi - 1));
-    if (f != INT_MAX) best[i] = BestEntry{0ull, static_cast<long long>(f)};
+    if (f != INT_MAX) {
+      best[i] = BestEntry{0ull, static_cast<long long>(f)};
+      continue;
+    }
+    int j = INT_MAX;
+    if (i - k_lo >= 0 && max(0, i - k_hi + 1) <= i - k_lo) j = max(0, i - k_hi + 1);
+    else if (i + k_lo <= L - 1) j = i + k_lo;
+    const unsigned long long one = static_cast<unsigned long long>(__double_as_longlong(1.0));
+    best[i] = (j == INT_MAX) ? BestEntry{kInfBits, kNoIdx} : BestEntry{one, static_cast<long long>(j)};
   }
 }
 
@@ -186,8 +203,10 @@ __global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__
                         int64_t* __restrict__ idx, int L) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
     const BestEntry e = best[i];
-    cmp[i] = __longlong_as_double(static_cast<long long>(e.v));
-    idx[i] = (e.v == kInfBits || e.idx == kNoIdx) ? -1 : e.idx;
+    const bool none = e.v == kInfBits || e.idx == kNoIdx || e.idx < 0;
+    cmp[i] = none ? __longlong_as_double(static_cast<long long>(kInfBits))
+                  : __longlong_as_double(static_cast<long long>(e.v));
+    idx[i] = none ? -1 : e.idx;
   }
 }
 
@@ -398,10 +417,11 @@ long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int num_s
     if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
     return L;  // the whole diagonal is one run, like the reference's refresh = 0
   }
-  long long R = std::max<long long>(16LL * (long long)cfg->m, 8LL * kS);
+  long long R = std::max<long long>(32LL * (long long)cfg->m, 8LL * kS);
   R = (R + kS - 1) / kS * kS;
   const long long want = 16LL * num_sms;
   while (R > 2 * kS && count_tiles(L, k_lo, k_hi, R) < want) R = std::max<long long>(2 * kS, (R / 2 + kS - 1) / kS * kS);
+  if (const char* e = getenv("MPROF_ROWS_PER_TILE")) R = std::max(1LL, atoll(e));  // experiments
   if (cfg->refresh_interval > 0) R = std::min<long long>(R, (long long)cfg->refresh_interval);
   return R;
 }
@@ -521,17 +541,21 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   if (st != MPROF_OK) return st;
   uint32_t launches = 0;
   const int g = grid_for(L);
-  k_init_best<<<g, 256, 0, c->stream>>>(w.best, L);
-  ++launches;
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
   if (zn) {
     c->stats_t = nullptr;  // force: the series bytes behind d_t may have changed
     st = ensure_znorm_stats(c, d_t, n64, cfg, w);
     if (st != MPROF_OK) return st;
+    k_init_best<<<g, 256, 0, c->stream>>>(w.best, w.B, L);
     k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
-    launches += 2;
+    launches += 3;
   } else {
-    k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m);
+    k_init_best<<<g, 256, 0, c->stream>>>(w.best, nullptr, L);
+    ++launches;
+    // the fast Euclidean policy slides (delta, sigma) pairs; everything else the raw pairs
+    const bool ds = !cfg->exact && (cfg->family == MPROF_EUCLIDEAN ||
+                                    (cfg->family == MPROF_PNORM && cfg->p == 2.0));
+    k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m, ds ? kPairsDeltaSum : kPairsRaw);
     ++launches;
   }
   CK(cudaGetLastError());

@@ -71,10 +71,23 @@ __device__ __forceinline__ unsigned long long offer(BestEntry* best, long long p
 // AAMP: A[p] = (t[p], t[p+m]); accumulator D^2.
 // Reference: incremental_euclidean_step (/root/reference/proj/include/mprof/aamp.hpp:37-42),
 // direct_sq_acc (/root/reference/proj/src/detail/diag_scan.hpp:57-64).
+// Operand layouts of A[p] (built by the host, see k_build_pairs / k_znorm_pairs):
+enum PairKind { kPairsRaw = 0, kPairsDeltaSum = 1, kPairsZnorm = 2 };
+
+// Fast-filter key of a cell: for distance-like accumulators the high word of the value (smaller
+// = better, monotone for non-negative doubles); see Znorm for the covariance key.
+__device__ __forceinline__ int hi_key(double v) { return __double2hiint(v); }
+
 template <bool EXACT>
 struct Euclid {
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
+  static constexpr bool kCovFilter = false;
+  // fast mode: A[p] = (delta_p, sigma_p) = (t[p+m] - t[p], t[p+m] + t[p]) and
+  //   in^2 - out^2 = (a' - b')^2 - (a - b)^2 = (delta_i - delta_j)(sigma_i - sigma_j),
+  // one DFMA + two DADD per cell instead of two DFMA + two DADD.
+  // exact mode: A[p] = (t[p], t[p+m]) and the reference's evaluation order.
+  static constexpr int kPairs = EXACT ? kPairsRaw : kPairsDeltaSum;
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     if constexpr (EXACT) {
       // max(0, acc - out*out + in*in), no contraction, clamp propagates (aamp.hpp:41)
@@ -83,11 +96,10 @@ struct Euclid {
       const double x = __dadd_rn(__dsub_rn(acc, __dmul_rn(out, out)), __dmul_rn(in, in));
       return (0.0 < x) ? x : 0.0;
     } else {
-      const double out = r.x - c.x;
-      const double in = r.y - c.y;
-      return fma(in, in, fma(-out, out, acc));
+      return fma(r.x - c.x, r.y - c.y, acc);
     }
   }
+  __device__ __forceinline__ static int key(double acc) { return hi_key(acc); }
   __device__ __forceinline__ static double score(double acc, double, double) { return acc; }
   __device__ __forceinline__ static double seed(double acc, double a, double b, double, double) {
     if constexpr (EXACT) {
@@ -116,6 +128,9 @@ template <int PK, bool EXACT>
 struct Pnorm {
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
+  static constexpr bool kCovFilter = false;
+  static constexpr int kPairs = kPairsRaw;
+  __device__ __forceinline__ static int key(double acc) { return hi_key(acc); }
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double p) {
     if constexpr (EXACT) {
       const double po = abs_pow_exact<PK>(__dsub_rn(r.x, c.x), p);
@@ -159,9 +174,18 @@ struct Pnorm {
 // This replaces the reference's five uncentred running sums (advance_stats + f_value,
 // /root/reference/proj/include/mprof/acamp.hpp:28-60): same profile, 4 FP64 ops per cell
 // instead of 16 flops + 3 divides, and no cancellation against the window level.
+//
+// Fast filter on the covariance alone (no per-cell normalisation): for a cell that can reach a
+// threshold tau (d <= tau < 1), cov >= (1 - tau) / (B_i B_j) >= (1 - tau_max) / (max B_r max B_c)
+// over the rows / columns of the thread's block, so the hot loop keeps only max(cov) — the key
+// ~hi(cov) is decreasing in cov — and the exact score is evaluated in the replay only:
+// 2 DFMA per cell.
 struct Znorm {
   static constexpr bool kHasB = true;
   static constexpr bool kCenteredSeed = true;
+  static constexpr bool kCovFilter = true;
+  static constexpr int kPairs = kPairsZnorm;
+  __device__ __forceinline__ static int key(double acc) { return ~__double2hiint(acc); }
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     return fma(r.x, c.y, fma(c.x, r.y, acc));
   }
@@ -206,6 +230,11 @@ struct SweepSmem {
   double rowB[2][HASB ? S : 2];                // B[i0 + 1 + x]
   int rowT[2][S];                              // hi32(best[i0 + 1 + x].v), exact
   int rowBM[2][S / D];                         // max of rowT over aligned blocks of D
+  // z-norm filter scales, rounded DOWN (a smaller scale only loosens the filter): per aligned
+  // block of D columns in a ring of RING/D blocks (filled once, when the block arrives) and per
+  // block of D rows of the stage.
+  float colIB[HASB ? G::RING / D : 1];         // <= 1 / max colB of the block
+  float rowIB[2][HASB ? S / D : 1];            // <= 1 / max rowB of the block
 };
 
 struct SweepParams {
@@ -358,24 +387,31 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
   using G = Geo<D, T, S>;
   const int xb = threadIdx.x * D;
   double2 cA[D];
-  double cB[D];
   {
     const int q0 = G::pad((X0 + xb) % G::RING);  // X0 + xb is a multiple of D: no wrap inside
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      cA[d] = sm.colA[q0 + d];
-      if constexpr (P::kHasB) cB[d] = sm.colB[q0 + d];
-    }
+    for (int d = 0; d < D; ++d) cA[d] = sm.colA[q0 + d];
   }
   const double2* rowA = sm.rowA[b];
-  const double* rowB = sm.rowB[b];
   for (int s = 0; s < cnt; s += D) {
     // the D operands entering during this block are contiguous in the ring: constant offsets
     const int qn = G::pad((X0 + s + xb + D) % G::RING);
     const double2* nA = &sm.colA[qn];
-    const double* nB = &sm.colB[P::kHasB ? qn : 0];
     const int cb = s / D + threadIdx.x;
-    const int theta = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
+    const int tmax = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
+    int theta = tmax;
+    if constexpr (P::kCovFilter) {
+      if (tmax >= 0x3FF00000) {
+        theta = INT_MAX;  // some threshold >= 1: any cell may qualify
+      } else {
+        const double num = 1.0 - __hiloint2double(tmax, -1);  // 1 - (upper bound of tau_max) > 0
+        const int cq = (X0 / D + cb) % (G::RING / D);
+        const float ic = fminf(sm.colIB[cq], sm.colIB[cq + 1 == G::RING / D ? 0 : cq + 1]);
+        const double th = num * static_cast<double>(sm.rowIB[b][s / D]) * static_cast<double>(ic) *
+                          (1.0 - 0x1p-40);  // margin for the rounding of th and of the replay score
+        theta = ~__double2hiint(th);
+      }
+    }
     Acc<P, D> acc0;
 #pragma unroll
     for (int d = 0; d < D; ++d) acc0.a[d] = acc[d];
@@ -385,21 +421,17 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
       if (GUARD && s + u >= cnt) break;
       const int x = s + u;
       const double2 r = rowA[x];
-      double rb = 0.0;
-      if constexpr (P::kHasB) rb = rowB[x];
       const int row = i0 + x + 1;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int sl = (d + u) % D;
         acc[d] = P::step(acc[d], r, cA[sl], p);
-        const double v = P::score(acc[d], rb, P::kHasB ? cB[sl] : 0.0);
-        int h = __double2hiint(v);
+        int h = P::key(acc[d]);
         if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
         hmin = min(hmin, h);
       }
       // slide the column ring: slot u (used by d = 0 this substep) takes the next operand
       cA[u] = nA[u];
-      if constexpr (P::kHasB) cB[u] = nB[u];
     }
     if (hmin <= theta)
       replay_block<P, D, G::RING>(acc0, s, cnt, i0, xb, kt, kend, L, p, X0, sm.colA, sm.colB,
@@ -409,7 +441,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
 
 // Block maxima of the freshly loaded thresholds (after the stage's cp.async completed).
 template <bool HASB, int D, int T, int S>
-__device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, int b) {
+__device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, int b, int X0) {
   using G = Geo<D, T, S>;
   using SM = SweepSmem<HASB, D, T, S>;
   for (int blk = threadIdx.x; blk < SM::NCB; blk += T) {
@@ -426,6 +458,30 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, in
 #pragma unroll
     for (int d = 0; d < D; ++d) mx = max(mx, sm.rowT[b][blk * D + d]);
     sm.rowBM[b][blk] = mx;
+  }
+  if constexpr (HASB) {
+    // B >= 0: the maximum high word bounds max B from above (low word all ones); its float,
+    // rounded up, and the reciprocal rounded down give a lower bound of 1 / max B.
+    auto inv_bound = [](int hmax) -> float {
+      return __frcp_rd(__double2float_ru(__hiloint2double(hmax, -1)));
+    };
+    const int first = (X0 == 0) ? 0 : (X0 + G::K) / D;  // column blocks that arrived for this stage
+    const int last = (X0 + G::NCOL) / D;
+    for (int bx = first + static_cast<int>(threadIdx.x); bx < last; bx += T) {
+      const int q = G::pad((bx * D) % G::RING);
+      const int* w = reinterpret_cast<const int*>(&sm.colB[q]);
+      int hmax = 0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) hmax = max(hmax, w[2 * d + 1]);
+      sm.colIB[bx % (G::RING / D)] = inv_bound(hmax);
+    }
+    for (int blk = threadIdx.x; blk < S / D; blk += T) {
+      const int* w = reinterpret_cast<const int*>(&sm.rowB[b][blk * D]);
+      int hmax = 0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) hmax = max(hmax, w[2 * d + 1]);
+      sm.rowIB[b][blk] = inv_bound(hmax);
+    }
   }
 }
 
@@ -560,7 +616,7 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    stage_block_max<P::kHasB, D, T, S>(sm, st & 1);
+    stage_block_max<P::kHasB, D, T, S>(sm, st & 1, s0);
     __syncthreads();
     const bool full = (cnt == S) && (kb + G::K <= prm.k_hi) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {

@@ -321,3 +321,45 @@ def test_bands_merge_to_full_profile(mp):
 def test_fp64_peak_is_plausible(mp):
     g, ms = mp.fp64_peak()
     assert 5e3 < g < 1e5, g  # GFLOP/s
+
+
+# ---- full-size BASELINE configurations (C4, C5): size-independent properties -------------------
+
+def _full_size_checks(mp, t, m, fam, P, I, rows=6, pairs=20000, tol=TOL):
+    L = P.size
+    assert np.all(np.isfinite(P)) and np.all(I >= 0) and np.all(np.abs(I - np.arange(L)) >= 1)
+    # every reported distance is the (long-double) distance of the reported pair
+    r = np.random.default_rng(1)
+    idx = r.choice(L, min(pairs, L), replace=False)
+    d = oracle.dist_exact(t, idx, I[idx], m, fam)
+    bound = ZN_ABS if fam == ZNORM else 0.0
+    assert np.all(within(P[idx], d, tol) | (np.abs(P[idx] - d) <= bound))
+    # sampled exact rows: full O(L m) long-double argmin
+    rr = r.choice(L, rows, replace=False)
+    best, arg = oracle.exact_rows(t, m, rr, fam)
+    assert np.all(within(P[rr], best, tol) | (np.abs(P[rr] - best) <= bound)), (P[rr], best)
+    dg = oracle.dist_exact(t, rr, I[rr], m, fam)
+    assert np.all(within(dg, best, tol) | (np.abs(dg - best) <= bound))
+
+
+@pytest.mark.slow
+def test_c4_full_aamp_acamp(mp):
+    t = W.c4()
+    m = 1024
+    P, I = gpu(mp, t, m)
+    _full_size_checks(mp, t, m, EUCLIDEAN, P, I)
+    # the injected 5x-variance window stands out (Fig. 1 story): a window holding the
+    # whole 500-sample anomaly has D^2 ~ (500*5 + (m-500)) steps^2, sqrt(2.95) = 1.72x the median
+    steps = np.diff(t)
+    a = int(np.argmax(np.convolve(steps ** 2, np.ones(500), "valid")))
+    assert np.max(P[max(0, a - m):a + 500]) > 1.5 * np.median(P)
+    P, I = gpu(mp, t, m, ZNORM)
+    _full_size_checks(mp, t, m, ZNORM, P, I)
+
+
+@pytest.mark.slow
+def test_c5_full_acamp(mp):
+    t = W.c5()
+    m = 512
+    P, I = gpu(mp, t, m, ZNORM)
+    _full_size_checks(mp, t, m, ZNORM, P, I, rows=4, pairs=10000)

@@ -1,0 +1,29 @@
+"""Sweep-kernel timings of the C4 engines (and optional C2/C3/C5), experiments only."""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1901_05708_b200 as mp  # noqa: E402
+from paper_1901_05708_b200 import workloads as W  # noqa: E402
+
+names = sys.argv[1:] or ["C4aamp", "C4acamp"]
+ctx = mp.Context(0)
+ctx.set_timing(True)
+out = {}
+for name in names:
+    c = W.CONFIGS[name]
+    t = c.gen()
+    kind = {"euclidean": mp.DistanceKind.euclidean(), "pnorm": mp.DistanceKind.pnorm(c.p),
+            "znorm": mp.DistanceKind.znormalized()}[c.family]
+    fn = {"euclidean": mp.aamp, "pnorm": mp.aamp_pnorm, "znorm": mp.acamp}[c.family]
+    cfg = mp.ProfileConfig(c.m, kind)
+    ts = mp.make_time_series(t)
+    ms = []
+    for r in range(4):
+        res = fn(ts, cfg, ctx=ctx)
+        ms.append(res.info.sweep_ms)
+    best = min(ms[1:])
+    out[name] = {"sweep_ms": round(best, 3), "cells_per_s": f"{res.info.cells / (best * 1e-3):.4e}",
+                 "tiles": res.info.tiles, "R": res.info.rows_per_tile}
+print(json.dumps(out))
