@@ -237,6 +237,7 @@ def main():
     stream.synchronize()
 
     sweep_ms = {e: [] for e in engines}
+    ops_per_cell = {}
     launches = [0]
 
     def step(record=True):
@@ -252,6 +253,7 @@ def main():
                                    P.data_ptr(), ctx=ctx)
                 if record:
                     sweep_ms[e].append(info.sweep_ms)
+                    ops_per_cell[e] = info.fp64_ops_per_cell
                     launches[0] += info.kernel_launches + 1
 
     for _ in range(args.warmup):
@@ -295,10 +297,16 @@ def main():
         fl = rank_cells * FLOPS_PER_CELL[e]
         flops_total += fl
         kern_s_total += avg_ms * 1e-3
-        per_engine[e] = {"sweep_ms": avg_ms, "cells_per_s_gpu": rank_cells / (avg_ms * 1e-3),
+        cps = rank_cells / (avg_ms * 1e-3)
+        ops = ops_per_cell.get(e) or None
+        per_engine[e] = {"sweep_ms": avg_ms, "cells_per_s_gpu": cps,
                          "flops_per_cell": FLOPS_PER_CELL[e],
                          "tflops": fl / (avg_ms * 1e-3) / 1e12,
-                         "frac_of_fp64_peak": fl / (avg_ms * 1e-3) / (peak_gflops * 1e9)}
+                         "frac_of_fp64_peak": fl / (avg_ms * 1e-3) / (peak_gflops * 1e9),
+                         # the kernel's own FP64-pipe instructions per cell (SASS-audited) and the
+                         # resulting pipe occupancy: peak instr/s = peak flops / 2 (DFMA = 2 flops)
+                         "fp64_instr_per_cell": ops,
+                         "fp64_pipe_frac": cps * ops / (peak_gflops * 1e9 / 2) if ops else None}
     achieved = flops_total / kern_s_total / 1e12
     prof = load_traffic() or {}
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_gflops / 1e3,
@@ -307,7 +315,11 @@ def main():
                 "peak_source": "measured live: mprof_fp64_peak (independent DFMA chains, 148 SMs, CUDA events)",
                 "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
                 "algorithmic_bytes_per_launch": 8 * n + 16 * L,
-                "note": "FP64-pipe bound (T and P/I are L2-resident: ~1e-4 B/cell); neither HBM nor tensor cores",
+                "note": ("FP64-pipe bound (T and P/I are L2-resident: ~1e-4 B/cell); neither HBM nor "
+                         "tensor cores. achieved/frac count SURVEY.md 8(d) algorithmic flops per cell "
+                         "(AAMP 6, ACAMP 8); the kernel issues fewer FP64 instructions per cell "
+                         "(per_engine.fp64_instr_per_cell) thanks to the (delta, sigma) and "
+                         "covariance-filter reformulations; fp64_pipe_frac is the pipe occupancy"),
                 "per_engine": per_engine}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -92,6 +92,8 @@ typedef struct mprof_run_info {
   uint64_t rows_per_tile;    /* run length R of each tile (seeded directly at its start) */
   uint32_t kernel_launches;  /* kernels launched by this call */
   float sweep_ms;            /* CUDA-event time of the sweep kernel alone (0 if not timed) */
+  float fp64_ops_per_cell;   /* FP64-pipe instructions the sweep kernel issues per cell */
+  float fp32_ops_per_cell;   /* FP32 instructions per cell (FP32 mode) */
 } mprof_run_info;
 
 typedef struct mprof_ctx mprof_ctx;

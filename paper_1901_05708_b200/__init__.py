@@ -209,7 +209,8 @@ class _Config(C.Structure):
 class RunInfo(C.Structure):
     _fields_ = [("cells", C.c_uint64), ("diagonals", C.c_uint64), ("tiles", C.c_uint64),
                 ("rows_per_tile", C.c_uint64), ("kernel_launches", C.c_uint32),
-                ("sweep_ms", C.c_float)]
+                ("sweep_ms", C.c_float), ("fp64_ops_per_cell", C.c_float),
+                ("fp32_ops_per_cell", C.c_float)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -43,6 +43,10 @@ constexpr int kD = MPROF_TILE_D;  // diagonals per thread
 constexpr int kT = MPROF_TILE_T;  // threads per CTA
 constexpr int kS = MPROF_TILE_S;  // rows per shared-memory stage
 constexpr int kK = kD * kT;
+// covariance-only z-norm filter when the mean min/max window-scale ratio over 2*kD windows is at
+// least this (calibrated on the BASELINE workloads: m=1024 0.983, m=512 0.967 -> cov-only is
+// faster; m=256 0.93 -> column-scaled is 1.8x faster)
+constexpr double kZnCovFilterMinSpread = 0.955;
 
 thread_local std::string g_last_error;
 
@@ -115,6 +119,29 @@ __global__ void k_znorm_pairs(const double* __restrict__ t, const double* __rest
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L - 1; p += gridDim.x * blockDim.x) {
     const double a = t[p], b = t[p + m];
     A[p] = make_double2(0.5 * (b - a), (b - mu[p + 1]) + (a - mu[p]));
+  }
+}
+
+// Spread of the window scales B inside the sweep's filter blocks: mean over windows of
+// 2*kD consecutive positions of min B / max B (flat windows skipped). Close to 1 (long windows)
+// the covariance-only z-norm filter is tight; lower, the per-cell column-scaled form wins.
+__global__ void k_bspread(const double* __restrict__ B, int L, double* out) {
+  double sum = 0.0, cnt = 0.0;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; (b + 1) * 2 * kD <= L; b += gridDim.x * blockDim.x) {
+    double mn = INFINITY, mx = 0.0;
+    for (int d = 0; d < 2 * kD; ++d) {
+      const double v = B[b * 2 * kD + d];
+      if (v > 0.0) { mn = fmin(mn, v); mx = fmax(mx, v); }
+    }
+    if (mx > 0.0) { sum += mn / mx; cnt += 1.0; }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], sum);
+    atomicAdd(&out[1], cnt);
   }
 }
 
@@ -325,6 +352,8 @@ struct mprof_ctx {
   const double* stats_t = nullptr;
   uint64_t stats_n = 0, stats_m = 0;
   double stats_thr = -1.0;
+  bool zn_colscale = false;  // z-norm filter form chosen for the current sweep
+  double* d_spread = nullptr;
 };
 
 namespace {
@@ -476,7 +505,8 @@ int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams&
                        long long ntiles, int k1, uint32_t* launches, float* ms) {
   const bool fd = !cfg->exact;
   if (cfg->family == MPROF_ZNORMALIZED)
-    return launch_sweep<Znorm>(c, prm, ntiles, k1, fd, launches, ms);
+    return c->zn_colscale ? launch_sweep<Znorm<true>>(c, prm, ntiles, k1, fd, launches, ms)
+                          : launch_sweep<Znorm<false>>(c, prm, ntiles, k1, fd, launches, ms);
   const bool pn = cfg->family == MPROF_PNORM;
   const double p = cfg->p;
   if (!pn || p == 2.0) {
@@ -549,6 +579,22 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     k_init_best<<<g, 256, 0, c->stream>>>(w.best, w.B, L);
     k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
     launches += 3;
+    // filter form for this series: MPROF_ZN_FILTER=cov|col overrides the measured choice
+    const char* force = getenv("MPROF_ZN_FILTER");
+    if (force && !strcmp(force, "cov")) {
+      c->zn_colscale = false;
+    } else if (force && !strcmp(force, "col")) {
+      c->zn_colscale = true;
+    } else {
+      if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
+      CK(cudaMemsetAsync(c->d_spread, 0, 2 * sizeof(double), c->stream));
+      k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.B, L, c->d_spread);
+      double h[2];
+      CK(cudaMemcpyAsync(h, c->d_spread, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      ++launches;
+      c->zn_colscale = !(h[1] > 0.0 && h[0] / h[1] >= kZnCovFilterMinSpread);
+    }
   } else {
     k_init_best<<<g, 256, 0, c->stream>>>(w.best, nullptr, L);
     ++launches;
@@ -608,6 +654,16 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   ++launches;
   CK(cudaGetLastError());
   if (info) {
+    // FP64-pipe instructions per cell of the hot loop (SASS-audited)
+    float ops = 4.f;
+    if (cfg->family == MPROF_ZNORMALIZED) ops = c->zn_colscale ? 3.125f : 2.f;
+    else if (cfg->exact) ops = (cfg->family == MPROF_PNORM && cfg->p != 1.0 && cfg->p != 2.0) ? 8.f : 6.f;
+    else if (cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0) ops = 3.f;
+    else if (cfg->p == 1.0) ops = 4.f;
+    else if (cfg->p == 3.0 || cfg->p == 4.0) ops = 6.f;
+    else ops = 0.f;  // generic pow: library call, not a fixed count
+    info->fp64_ops_per_cell = ops;
+    info->fp32_ops_per_cell = 0.f;
     info->cells = cells;
     info->diagonals = k_hi > k_lo ? (uint64_t)(k_hi - k_lo) : 0;
     info->tiles = (uint64_t)ntiles;
@@ -739,6 +795,7 @@ void mprof_ctx_destroy(mprof_ctx* c) {
   if (c->ws) cudaFree(c->ws);
   if (c->io) cudaFree(c->io);
   if (c->tiles_d) cudaFree(c->tiles_d);
+  if (c->d_spread) cudaFree(c->d_spread);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

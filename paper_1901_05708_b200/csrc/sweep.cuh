@@ -83,6 +83,7 @@ struct Euclid {
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
   static constexpr bool kCovFilter = false;
+  static constexpr bool kColScale = false;
   // fast mode: A[p] = (delta_p, sigma_p) = (t[p+m] - t[p], t[p+m] + t[p]) and
   //   in^2 - out^2 = (a' - b')^2 - (a - b)^2 = (delta_i - delta_j)(sigma_i - sigma_j),
   // one DFMA + two DADD per cell instead of two DFMA + two DADD.
@@ -129,6 +130,7 @@ struct Pnorm {
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
   static constexpr bool kCovFilter = false;
+  static constexpr bool kColScale = false;
   static constexpr int kPairs = kPairsRaw;
   __device__ __forceinline__ static int key(double acc) { return hi_key(acc); }
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double p) {
@@ -180,10 +182,13 @@ struct Pnorm {
 // over the rows / columns of the thread's block, so the hot loop keeps only max(cov) — the key
 // ~hi(cov) is decreasing in cov — and the exact score is evaluated in the replay only:
 // 2 DFMA per cell.
+// COLSCALE selects the filter form (see run_stage): 0 = covariance only, 1 = cov * B_j.
+template <bool COLSCALE>
 struct Znorm {
   static constexpr bool kHasB = true;
   static constexpr bool kCenteredSeed = true;
   static constexpr bool kCovFilter = true;
+  static constexpr bool kColScale = COLSCALE;
   static constexpr int kPairs = kPairsZnorm;
   __device__ __forceinline__ static int key(double acc) { return ~__double2hiint(acc); }
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
@@ -235,6 +240,7 @@ struct SweepSmem {
   // block of D rows of the stage.
   float colIB[HASB ? G::RING / D : 1];         // <= 1 / max colB of the block
   float rowIB[2][HASB ? S / D : 1];            // <= 1 / max rowB of the block
+  float rowIBx[2][HASB ? S : 1];               // <= 1 / rowB of each row
 };
 
 struct SweepParams {
@@ -294,15 +300,35 @@ struct Acc {
   double a[D];
 };
 
-template <class P, int D, int RING>
-__device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0, int xb, int kt,
-                                          int kend, int L, double p, int X0, const double2* colA,
-                                          const double* colB, int* colT, const double2* rowA,
-                                          const double* rowB, int* rowT, BestEntry* best,
-                                          unsigned long long* stats) {
-  using G = Geo<D, 1, 1>;
+// Exact merge of one flagged cell (rarely reached): column entry first, then the row candidate.
+__device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhit, int row, int j,
+                                        int* ct, BestEntry* best, unsigned long long* rv, int* rj,
+                                        unsigned long long* stats) {
+  // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
+  const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+  if (colhit) {
+    atomicMin(ct, static_cast<int>(offer(best, j, vb, row) >> 32));
+    if (stats) atomicAdd(&stats[1], 1ull);
+  }
+  if (rowhit && lex_less(vb, j, *rv, *rj)) {
+    *rv = vb;
+    *rj = j;
+  }
+}
+
+// The replay of one block (D sub-steps x D diagonals of one lane), fully unrolled. The 2D-1
+// column operands of the block are two aligned runs of D in the ring (c1 = X0+s+xb, c2 = +D) and
+// the thresholds two aligned runs in the stage buffer; cell (u, d) uses run entry u + d.
+template <class P, int D, bool GUARD>
+__device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0, int kt, int kend,
+                                          int L, double p, const double2* cA1, const double2* cA2,
+                                          const double* cB1, const double* cB2, int* cT1,
+                                          int* cT2, const double2* rowA, const double* rowB,
+                                          int* rowT, BestEntry* best, unsigned long long* stats) {
   if (stats) atomicAdd(&stats[0], 1ull);
-  for (int u = 0; u < D && s + u < cnt; ++u) {
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+    if (GUARD && s + u >= cnt) break;
     const int x = s + u;
     const double2 r = rowA[x];
     const double rb = P::kHasB ? rowB[x] : 0.0;
@@ -312,26 +338,16 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
     int rj = INT_MAX;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int q = G::pad((X0 + x + xb + d) % RING);
-      acc.a[d] = P::step(acc.a[d], r, colA[q], p);
-      const double v = P::score(acc.a[d], rb, P::kHasB ? colB[q] : 0.0);
-      if (!((kt + d < kend) && (row + kt + d <= L - 1))) continue;
+      const int e = u + d;  // entry of the block's column run
+      const double2 c = e < D ? cA1[e] : cA2[e - D];
+      acc.a[d] = P::step(acc.a[d], r, c, p);
+      const double v = P::score(acc.a[d], rb, P::kHasB ? (e < D ? cB1[e] : cB2[e - D]) : 0.0);
+      if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) continue;
       const int h = __double2hiint(v);
-      int* ct = &colT[G::pad(x + xb + d)];
+      int* ct = e < D ? &cT1[e] : &cT2[e - D];
       const bool rowhit = h <= tr;
       const bool colhit = h <= *reinterpret_cast<volatile int*>(ct);
-      if (!(rowhit || colhit)) continue;
-      // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
-      const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
-      const int j = row + kt + d;
-      if (colhit) {
-        atomicMin(ct, static_cast<int>(offer(best, j, vb, row) >> 32));
-        if (stats) atomicAdd(&stats[1], 1ull);
-      }
-      if (rowhit && lex_less(vb, j, rv, rj)) {
-        rv = vb;
-        rj = j;
-      }
+      if (rowhit || colhit) merge_cell(v, h, rowhit, colhit, row, row + kt + d, ct, best, &rv, &rj, stats);
     }
     if (rj != INT_MAX) {
       atomicMin(&rowT[x], static_cast<int>(offer(best, row, rv, rj) >> 32));
@@ -385,57 +401,88 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
                                           int L, BestEntry* best, double p,
                                           unsigned long long* stats) {
   using G = Geo<D, T, S>;
+  // z-norm filter form: 0 = covariance only vs a block bound (2 DFMA per cell; loose when the
+  // window scales B vary inside a block, e.g. short windows); 1 = cov * B_j per cell vs a per-row
+  // bound (2 DFMA + 1 DMUL per cell; tight up to the block's max threshold).
+  constexpr bool kColScale = P::kColScale;
   const int xb = threadIdx.x * D;
   double2 cA[D];
+  double cB[D];
   {
     const int q0 = G::pad((X0 + xb) % G::RING);  // X0 + xb is a multiple of D: no wrap inside
 #pragma unroll
-    for (int d = 0; d < D; ++d) cA[d] = sm.colA[q0 + d];
+    for (int d = 0; d < D; ++d) {
+      cA[d] = sm.colA[q0 + d];
+      if constexpr (kColScale) cB[d] = sm.colB[q0 + d];
+    }
   }
   const double2* rowA = sm.rowA[b];
   for (int s = 0; s < cnt; s += D) {
     // the D operands entering during this block are contiguous in the ring: constant offsets
     const int qn = G::pad((X0 + s + xb + D) % G::RING);
     const double2* nA = &sm.colA[qn];
+    const double* nB = &sm.colB[P::kHasB ? qn : 0];
     const int cb = s / D + threadIdx.x;
     const int tmax = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
     int theta = tmax;
+    double num = 0.0;  // kColScale: 1 - tau_max (with margin), 0 = every cell may qualify
     if constexpr (P::kCovFilter) {
       if (tmax >= 0x3FF00000) {
         theta = INT_MAX;  // some threshold >= 1: any cell may qualify
       } else {
-        const double num = 1.0 - __hiloint2double(tmax, -1);  // 1 - (upper bound of tau_max) > 0
-        const int cq = (X0 / D + cb) % (G::RING / D);
-        const float ic = fminf(sm.colIB[cq], sm.colIB[cq + 1 == G::RING / D ? 0 : cq + 1]);
-        const double th = num * static_cast<double>(sm.rowIB[b][s / D]) * static_cast<double>(ic) *
-                          (1.0 - 0x1p-40);  // margin for the rounding of th and of the replay score
-        theta = ~__double2hiint(th);
+        num = (1.0 - __hiloint2double(tmax, -1)) * (1.0 - 0x1p-40);  // margin for roundings
+        if constexpr (!kColScale) {
+          const int cq = (X0 / D + cb) % (G::RING / D);
+          const float ic = fminf(sm.colIB[cq], sm.colIB[cq + 1 == G::RING / D ? 0 : cq + 1]);
+          const double th = num * static_cast<double>(sm.rowIB[b][s / D]) * static_cast<double>(ic);
+          theta = ~__double2hiint(th);
+        }
       }
     }
     Acc<P, D> acc0;
 #pragma unroll
     for (int d = 0; d < D; ++d) acc0.a[d] = acc[d];
     int hmin = INT_MAX;
+    bool hit = false;
 #pragma unroll
     for (int u = 0; u < D; ++u) {
       if (GUARD && s + u >= cnt) break;
       const int x = s + u;
       const double2 r = rowA[x];
       const int row = i0 + x + 1;
+      int hu = INT_MAX;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int sl = (d + u) % D;
         acc[d] = P::step(acc[d], r, cA[sl], p);
-        int h = P::key(acc[d]);
+        int h;
+        if constexpr (kColScale) h = ~__double2hiint(acc[d] * cB[sl]);
+        else h = P::key(acc[d]);
         if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
-        hmin = min(hmin, h);
+        hu = min(hu, h);
+      }
+      if constexpr (kColScale) {
+        // row bound for this sub-step: cov * B_j >= (1 - tau) / B_i
+        const int tu = (num == 0.0) ? INT_MAX
+                                    : ~__double2hiint(num * static_cast<double>(sm.rowIBx[b][x]));
+        hit |= hu <= tu;
+      } else {
+        hmin = min(hmin, hu);
       }
       // slide the column ring: slot u (used by d = 0 this substep) takes the next operand
       cA[u] = nA[u];
+      if constexpr (kColScale) cB[u] = nB[u];
     }
-    if (hmin <= theta)
-      replay_block<P, D, G::RING>(acc0, s, cnt, i0, xb, kt, kend, L, p, X0, sm.colA, sm.colB,
-                                  sm.colT[b], sm.rowA[b], sm.rowB[b], sm.rowT[b], best, stats);
+    if constexpr (!kColScale) hit = hmin <= theta;
+    if (hit) {
+      const int q1 = G::pad((X0 + s + xb) % G::RING);
+      const int q2 = G::pad((X0 + s + xb + D) % G::RING);
+      int* colT = sm.colT[b];
+      replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, p, &sm.colA[q1], &sm.colA[q2],
+                                &sm.colB[P::kHasB ? q1 : 0], &sm.colB[P::kHasB ? q2 : 0],
+                                &colT[G::pad(s + xb)], &colT[G::pad(s + xb + D)], rowA,
+                                sm.rowB[b], sm.rowT[b], best, stats);
+    }
   }
 }
 
@@ -475,6 +522,8 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, in
       for (int d = 0; d < D; ++d) hmax = max(hmax, w[2 * d + 1]);
       sm.colIB[bx % (G::RING / D)] = inv_bound(hmax);
     }
+    for (int x = threadIdx.x; x < S; x += T)
+      sm.rowIBx[b][x] = inv_bound(reinterpret_cast<const int*>(&sm.rowB[b][x])[1]);
     for (int blk = threadIdx.x; blk < S / D; blk += T) {
       const int* w = reinterpret_cast<const int*>(&sm.rowB[b][blk * D]);
       int hmax = 0;

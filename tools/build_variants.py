@@ -15,8 +15,8 @@ OUT = ROOT / "build" / "variants"
 
 
 def one(spec):
-    D, T, S, MB = spec.split(",")
-    tag = f"d{D}_t{T}_s{S}_b{MB}"
+    D, T, S, MB, *extra = spec.split(",")
+    tag = f"d{D}_t{T}_s{S}_b{MB}" + "".join("_" + e.replace("=", "").replace("MPROF_", "").lower() for e in extra)
     objdir = OUT / tag
     objdir.mkdir(parents=True, exist_ok=True)
     objs = []
@@ -24,6 +24,7 @@ def one(spec):
         obj = objdir / (src.name + ".o")
         B._run([B.NVCC, *B.NVFLAGS, *B.ARCH, "-I", str(ROOT / "include"), f"-DMPROF_TILE_D={D}",
                 f"-DMPROF_TILE_T={T}", f"-DMPROF_TILE_S={S}", f"-DMPROF_MIN_BLOCKS={MB}",
+                *[f"-D{e}" for e in extra],
                 "-c", str(src), "-o", str(obj)])
         objs.append(str(obj))
     lib = OUT / f"libmprof_gpu_{tag}.so"
