@@ -122,6 +122,34 @@ __global__ void k_znorm_pairs(const double* __restrict__ t, const double* __rest
   }
 }
 
+// FP32 mode operands (sweep.cuh, *F32 policies). c = series mean (device scalar) is the offset
+// that keeps float's digits where the differences are: DeltaSum (delta, sigma - 2c), Raw
+// (t - c, t[p+m] - c); z-norm (df, dg) and B are offset-free.
+__global__ void k_mean(const double* __restrict__ t, int n, double* out) {
+  double s = 0.0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) s += t[p];
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s / n);
+}
+
+__global__ void k_build_pairs32(const double* __restrict__ t, float2* __restrict__ A, int L, int m,
+                                int kind, const double* __restrict__ mean) {
+  const double c = *mean;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L - 1; p += gridDim.x * blockDim.x) {
+    const double a = t[p], b = t[p + m];
+    A[p] = kind == kPairsDeltaSum ? make_float2((float)(b - a), (float)((b - c) + (a - c)))
+                                  : make_float2((float)(a - c), (float)(b - c));
+  }
+}
+
+__global__ void k_znorm_pairs32(const double2* __restrict__ A, const double* __restrict__ B,
+                                float2* __restrict__ A32, float* __restrict__ B32, int L) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
+    if (p < L - 1) A32[p] = make_float2((float)A[p].x, (float)A[p].y);
+    B32[p] = (float)B[p];
+  }
+}
+
 // Spread of the window scales B inside the sweep's filter blocks: mean over windows of
 // 2*kD consecutive positions of min B / max B (flat windows skipped). Close to 1 (long windows)
 // the covariance-only z-norm filter is tight; lower, the per-cell column-scaled form wins.
@@ -148,8 +176,9 @@ __global__ void k_bspread(const double* __restrict__ B, int L, double* out) {
 // Thresholds from the band's first diagonal k1: every cell (i, i+k1) evaluated directly and
 // merged exactly. These are genuine cells of the band, so the result is unchanged; they only
 // give the high-word filter near-final thresholds before the tiles start.
-template <class P>
+template <class PP>
 __global__ void k_first_diag(SweepParams prm, int k1) {
+  using P = typename PP::Base;  // FP64 evaluation, also in FP32 mode
   const int L = prm.L;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + k1 <= L - 1;
        i += gridDim.x * blockDim.x) {
@@ -399,6 +428,9 @@ struct Workspace {
   double* mu;
   BestEntry* best;
   int* cmin;
+  float2* A32;
+  float* B32;
+  double* scalars;  // [0] series mean (FP32 offset)
 };
 
 int32_t carve(mprof_ctx* c, int L, Workspace* w) {
@@ -406,7 +438,10 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   const size_t nB = align_up(sizeof(double) * (size_t)L);
   const size_t nBest = align_up(sizeof(BestEntry) * (size_t)L);
   const size_t nC = align_up(sizeof(int) * ((size_t)L / kChunk + 2));
-  const int32_t st = ensure(&c->ws, &c->ws_bytes, nA + 2 * nB + nBest + nC);
+  const size_t nA32 = align_up(sizeof(float2) * (size_t)L);
+  const size_t nB32 = align_up(sizeof(float) * (size_t)L);
+  const size_t nS = align_up(8 * sizeof(double));
+  const int32_t st = ensure(&c->ws, &c->ws_bytes, nA + 2 * nB + nBest + nC + nA32 + nB32 + nS);
   if (st != MPROF_OK) return st;
   char* base = static_cast<char*>(c->ws);
   w->A = reinterpret_cast<double2*>(base);
@@ -414,6 +449,9 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   w->mu = reinterpret_cast<double*>(base + nA + nB);
   w->best = reinterpret_cast<BestEntry*>(base + nA + 2 * nB);
   w->cmin = reinterpret_cast<int*>(base + nA + 2 * nB + nBest);
+  w->A32 = reinterpret_cast<float2*>(base + nA + 2 * nB + nBest + nC);
+  w->B32 = reinterpret_cast<float*>(base + nA + 2 * nB + nBest + nC + nA32);
+  w->scalars = reinterpret_cast<double*>(base + nA + 2 * nB + nBest + nC + nA32 + nB32);
   return MPROF_OK;
 }
 
@@ -479,7 +517,7 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, long long R, long l
 template <class P>
 int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int k1,
                      bool first_diag, uint32_t* launches, float* ms) {
-  using SM = SweepSmem<P::kHasB, kD, kT, kS>;
+  using SM = SweepSmem<P, kD, kT, kS>;
   const size_t smem = sizeof(SM);
   auto kern = sweep_kernel<P, kD, kT, kS, MPROF_MIN_BLOCKS>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -504,6 +542,18 @@ int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int
 int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
                        long long ntiles, int k1, uint32_t* launches, float* ms) {
   const bool fd = !cfg->exact;
+  if (cfg->precision == MPROF_FP32) {
+    if (cfg->family == MPROF_ZNORMALIZED)
+      return c->zn_colscale ? launch_sweep<ZnormF32<true>>(c, prm, ntiles, k1, fd, launches, ms)
+                            : launch_sweep<ZnormF32<false>>(c, prm, ntiles, k1, fd, launches, ms);
+    const double p = cfg->p;
+    if (cfg->family == MPROF_EUCLIDEAN || p == 2.0)
+      return launch_sweep<EuclidF32>(c, prm, ntiles, k1, fd, launches, ms);
+    if (p == 1.0) return launch_sweep<PnormF32<1>>(c, prm, ntiles, k1, fd, launches, ms);
+    if (p == 3.0) return launch_sweep<PnormF32<3>>(c, prm, ntiles, k1, fd, launches, ms);
+    if (p == 4.0) return launch_sweep<PnormF32<4>>(c, prm, ntiles, k1, fd, launches, ms);
+    return launch_sweep<PnormF32<0>>(c, prm, ntiles, k1, fd, launches, ms);
+  }
   if (cfg->family == MPROF_ZNORMALIZED)
     return c->zn_colscale ? launch_sweep<Znorm<true>>(c, prm, ntiles, k1, fd, launches, ms)
                           : launch_sweep<Znorm<false>>(c, prm, ntiles, k1, fd, launches, ms);
@@ -557,7 +607,8 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
                    mprof_run_info* info) {
   int32_t st = check_config(n64, cfg);
   if (st != MPROF_OK) return st;
-  if (cfg->precision == MPROF_FP32) return fail(MPROF_E_BAD_ARG, "FP32 mode not built yet");
+  if (cfg->precision == MPROF_FP32 && cfg->exact)
+    return fail(MPROF_E_BAD_ARG, "the exact (parity) mode is FP64 only");
   const int n = (int)n64, m = (int)cfg->m;
   const int L = n - m + 1;
   // band: [max(k_lo, excl), min(k_hi, L)) ; 0,0 = everything
@@ -604,6 +655,19 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m, ds ? kPairsDeltaSum : kPairsRaw);
     ++launches;
   }
+  if (cfg->precision == MPROF_FP32) {
+    if (zn) {
+      k_znorm_pairs32<<<g, 256, 0, c->stream>>>(w.A, w.B, w.A32, w.B32, L);
+      ++launches;
+    } else {
+      CK(cudaMemsetAsync(w.scalars, 0, sizeof(double), c->stream));
+      k_mean<<<grid_for(n), 256, 0, c->stream>>>(d_t, n, w.scalars);
+      const bool ds32 = cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0;
+      k_build_pairs32<<<g, 256, 0, c->stream>>>(d_t, w.A32, L, m, ds32 ? kPairsDeltaSum : kPairsRaw,
+                                                w.scalars);
+      launches += 2;
+    }
+  }
   CK(cudaGetLastError());
   float ms = 0.f;
   long long ntiles = 0, R = 0;
@@ -616,6 +680,8 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     prm.t = d_t;
     prm.A = w.A;
     prm.B = w.B;
+    prm.A32 = w.A32;
+    prm.B32 = w.B32;
     prm.mu = w.mu;
     prm.best = w.best;
     prm.tiles = c->tiles_d;
@@ -662,8 +728,13 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     else if (cfg->p == 1.0) ops = 4.f;
     else if (cfg->p == 3.0 || cfg->p == 4.0) ops = 6.f;
     else ops = 0.f;  // generic pow: library call, not a fixed count
-    info->fp64_ops_per_cell = ops;
-    info->fp32_ops_per_cell = 0.f;
+    if (cfg->precision == MPROF_FP32) {
+      info->fp64_ops_per_cell = 0.f;
+      info->fp32_ops_per_cell = ops;
+    } else {
+      info->fp64_ops_per_cell = ops;
+      info->fp32_ops_per_cell = 0.f;
+    }
     info->cells = cells;
     info->diagonals = k_hi > k_lo ? (uint64_t)(k_hi - k_lo) : 0;
     info->tiles = (uint64_t)ntiles;

@@ -5,23 +5,23 @@
 // (/root/reference/proj/src/detail/diag_scan.hpp:193-259), with MinBuffer's lexicographic
 // (value, index) minimum (diag_scan.hpp:31-53).
 //
-// B200 design (see DESIGN.md for the full derivation):
+// B200 design (DESIGN.md §3 has the derivation and the measurements):
 //  * A CTA owns a TILE = K = T*D consecutive diagonals x R consecutive rows. Thread `tid` owns
-//    D consecutive diagonals and walks the rows, so a cell costs only the O(1) slide
-//    (4 FP64-pipe instructions for AAMP, p=1 and ACAMP) and each tile is seeded with one direct
-//    length-m sum per diagonal (the reference's refresh rule, diag_scan.hpp:93-105, is exactly
-//    "seed at multiples of R").
-//  * Per-position operands are staged in shared memory per STAGE of S rows with cp.async,
-//    double-buffered. Every thread reads a new column operand per row into a register ring of
-//    D slots (compile-time rotation, no moves); row operands are warp broadcasts. The column
-//    arrays are padded (x + x/D) so the stride-D lane pattern is bank-conflict free.
+//    D consecutive diagonals and walks the rows; each tile is seeded with one direct length-m
+//    sum per diagonal (the reference's refresh rule, diag_scan.hpp:93-105, is exactly "seed at
+//    multiples of R"), then every cell costs the O(1) slide: 3 FP64-pipe instructions for AAMP
+//    ((delta, sigma) form), 2 or 3 for ACAMP (centred covariance, covariance filter).
+//  * Column operands stream through a shared-memory RING (cp.async), one new operand per thread
+//    per row into a register ring of D slots with compile-time rotation; row operands are warp
+//    broadcasts; padding x -> x + x/D keeps the stride-D lane pattern bank-conflict free.
 //  * Minima: the exact global profile is an array of 16-byte (value bits, index) entries merged
 //    with a 128-bit atomicCAS lexicographic minimum (MinBuffer::update semantics). The hot loop
-//    never touches it: each cell is compared, as a signed 32-bit integer, against the HIGH word
-//    of the current row and column minima (for non-negative doubles the high word is monotone),
-//    which is one ISETP per side. Only cells whose high word is <= a threshold (a possible
-//    improvement or tie) take the exact slow path (`resolve`). Row candidates are warp-reduced
-//    before touching global memory.
+//    never touches it: per block of D sub-steps it keeps the minimum 32-bit key of its cells
+//    and compares it once with the block's maximum threshold; a passing block is replayed
+//    bit-identically through the exact slow path.
+//  * FP32 mode: the same machinery with float accumulators/operands (policies *F32); values are
+//    promoted exactly to double for the merge, and finalize recomputes the reported distance of
+//    the chosen pair in FP64.
 #pragma once
 
 #include <cstdint>
@@ -66,28 +66,50 @@ __device__ __forceinline__ unsigned long long offer(BestEntry* best, long long p
 // Distance families ("policies"). A[p] is the per-position operand pair, B[p] an optional
 // per-position scalar (the z-normalization scale). step() slides the diagonal accumulator from
 // cell (i, j) to (i+1, j+1) using A[i] (row) and A[j] (column); score() maps the accumulator of
-// the new cell to the comparison value using B[i+1], B[j+1]. Seeds are direct length-m sums.
+// the new cell to the comparison value using B[i+1], B[j+1]; key() is the 32-bit fast-filter
+// key (smaller = better). Seeds are direct length-m sums, always in FP64.
 
-// AAMP: A[p] = (t[p], t[p+m]); accumulator D^2.
-// Reference: incremental_euclidean_step (/root/reference/proj/include/mprof/aamp.hpp:37-42),
-// direct_sq_acc (/root/reference/proj/src/detail/diag_scan.hpp:57-64).
 // Operand layouts of A[p] (built by the host, see k_build_pairs / k_znorm_pairs):
 enum PairKind { kPairsRaw = 0, kPairsDeltaSum = 1, kPairsZnorm = 2 };
 
-// Fast-filter key of a cell: for distance-like accumulators the high word of the value (smaller
-// = better, monotone for non-negative doubles); see Znorm for the covariance key.
-__device__ __forceinline__ int hi_key(double v) { return __double2hiint(v); }
+// Threshold words are high words of FP64 comparison values. FP64 keys compare with them
+// directly; FP32 keys are float bits, so a threshold is converted to the float bound rounded UP
+// (a looser filter is always safe: the replay decides exactly).
+struct KeyF64 {
+  __device__ __forceinline__ static int key(double v) { return __double2hiint(v); }
+  __device__ __forceinline__ static int tau(int hi) { return hi; }
+  // covariance-filter key and bound (larger covariance = better): ~hi is decreasing
+  __device__ __forceinline__ static int cov_key(double c) { return ~__double2hiint(c); }
+  __device__ __forceinline__ static int cov_bound(double th) { return ~__double2hiint(th); }
+};
+struct KeyF32 {
+  __device__ __forceinline__ static int key(float v) { return __float_as_int(v); }
+  __device__ __forceinline__ static int tau(int hi) {
+    if (hi >= 0x47EFFFFF) return INT_MAX;  // at or beyond FLT_MAX (incl. +inf): pass everything
+    return __float_as_int(__double2float_ru(__hiloint2double(hi, -1)));
+  }
+  __device__ __forceinline__ static int cov_key(float c) { return ~__float_as_int(c); }
+  __device__ __forceinline__ static int cov_bound(double th) {
+    return ~__float_as_int(__double2float_rd(th));
+  }
+};
 
+// AAMP. Reference: incremental_euclidean_step (/root/reference/proj/include/mprof/aamp.hpp:37-42),
+// direct_sq_acc (/root/reference/proj/src/detail/diag_scan.hpp:57-64).
+// fast mode: A[p] = (delta_p, sigma_p) = (t[p+m] - t[p], t[p+m] + t[p]) and
+//   in^2 - out^2 = (a' - b')^2 - (a - b)^2 = (delta_i - delta_j)(sigma_i - sigma_j),
+// one DFMA + two DADD per cell instead of two DFMA + two DADD.
+// exact mode: A[p] = (t[p], t[p+m]) and the reference's evaluation order.
 template <bool EXACT>
-struct Euclid {
+struct Euclid : KeyF64 {
+  using Base = Euclid;  // FP64 policy used by the first-diagonal pre-pass
+  using V = double;
+  using V2 = double2;
+  using VB = double;
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
   static constexpr bool kCovFilter = false;
   static constexpr bool kColScale = false;
-  // fast mode: A[p] = (delta_p, sigma_p) = (t[p+m] - t[p], t[p+m] + t[p]) and
-  //   in^2 - out^2 = (a' - b')^2 - (a - b)^2 = (delta_i - delta_j)(sigma_i - sigma_j),
-  // one DFMA + two DADD per cell instead of two DFMA + two DADD.
-  // exact mode: A[p] = (t[p], t[p+m]) and the reference's evaluation order.
   static constexpr int kPairs = EXACT ? kPairsRaw : kPairsDeltaSum;
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     if constexpr (EXACT) {
@@ -100,7 +122,6 @@ struct Euclid {
       return fma(r.x - c.x, r.y - c.y, acc);
     }
   }
-  __device__ __forceinline__ static int key(double acc) { return hi_key(acc); }
   __device__ __forceinline__ static double score(double acc, double, double) { return acc; }
   __device__ __forceinline__ static double seed(double acc, double a, double b, double, double) {
     if constexpr (EXACT) {
@@ -126,13 +147,16 @@ __device__ __forceinline__ double abs_pow_exact(double x, double p) {
 // p-norm AAMP: accumulator sum |t_i - t_j|^p. PK = 1, 3, 4 integer fast paths; 0 = generic pow.
 // Reference: incremental_pnorm_step (aamp.hpp:45-49), direct_pnorm_acc (diag_scan.hpp:66-71).
 template <int PK, bool EXACT>
-struct Pnorm {
+struct Pnorm : KeyF64 {
+  using Base = Pnorm;
+  using V = double;
+  using V2 = double2;
+  using VB = double;
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
   static constexpr bool kCovFilter = false;
   static constexpr bool kColScale = false;
   static constexpr int kPairs = kPairsRaw;
-  __device__ __forceinline__ static int key(double acc) { return hi_key(acc); }
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double p) {
     if constexpr (EXACT) {
       const double po = abs_pow_exact<PK>(__dsub_rn(r.x, c.x), p);
@@ -174,23 +198,23 @@ struct Pnorm {
 // dg_p = (t[p+m]-mu_{p+1}) + (t[p]-mu_p)  (A[p] = (df_p, dg_p)), and B[p] = 1/||t_p - mu_p||
 // (0 for flat windows). Comparison value d = 1 - corr = 1 - cov*B[i]*B[j], DZ^2 = 2m*d.
 // This replaces the reference's five uncentred running sums (advance_stats + f_value,
-// /root/reference/proj/include/mprof/acamp.hpp:28-60): same profile, 4 FP64 ops per cell
-// instead of 16 flops + 3 divides, and no cancellation against the window level.
-//
-// Fast filter on the covariance alone (no per-cell normalisation): for a cell that can reach a
-// threshold tau (d <= tau < 1), cov >= (1 - tau) / (B_i B_j) >= (1 - tau_max) / (max B_r max B_c)
-// over the rows / columns of the thread's block, so the hot loop keeps only max(cov) — the key
-// ~hi(cov) is decreasing in cov — and the exact score is evaluated in the replay only:
-// 2 DFMA per cell.
-// COLSCALE selects the filter form (see run_stage): 0 = covariance only, 1 = cov * B_j.
+// /root/reference/proj/include/mprof/acamp.hpp:28-60): same profile, no divide, and no
+// cancellation against the window level.
+// Fast filter (run_stage): for a cell that can reach a threshold tau < 1,
+// cov * B_i * B_j >= 1 - tau, so the hot loop tests cov alone against a block bound
+// (COLSCALE = 0: 2 DFMA per cell) or cov * B_j against a per-row bound (COLSCALE = 1:
+// + 1 DMUL per cell, tight when the window scales vary, e.g. short windows).
 template <bool COLSCALE>
-struct Znorm {
+struct Znorm : KeyF64 {
+  using Base = Znorm;
+  using V = double;
+  using V2 = double2;
+  using VB = double;
   static constexpr bool kHasB = true;
   static constexpr bool kCenteredSeed = true;
   static constexpr bool kCovFilter = true;
   static constexpr bool kColScale = COLSCALE;
   static constexpr int kPairs = kPairsZnorm;
-  __device__ __forceinline__ static int key(double acc) { return ~__double2hiint(acc); }
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     return fma(r.x, c.y, fma(c.x, r.y, acc));
   }
@@ -204,8 +228,81 @@ struct Znorm {
   }
 };
 
+// ---- FP32 mode policies ------------------------------------------------------------------------
+// Same slides in float; seeds in FP64 (rounded once to float). Operands are built relative to a
+// global offset c (the series mean) so that float keeps the digits that matter: AAMP
+// A = (delta, sigma - 2c), p-norm A = (t - c, t[p+m] - c); ACAMP's (df, dg) and B are
+// offset-free. Comparison values are promoted exactly to double for the merge.
+
+struct EuclidF32 : KeyF32 {
+  using Base = Euclid<false>;
+  using V = float;
+  using V2 = float2;
+  using VB = float;
+  static constexpr bool kHasB = false;
+  static constexpr bool kCenteredSeed = false;
+  static constexpr bool kCovFilter = false;
+  static constexpr bool kColScale = false;
+  static constexpr int kPairs = kPairsDeltaSum;
+  __device__ __forceinline__ static float step(float acc, float2 r, float2 c, double) {
+    return fmaf(r.x - c.x, r.y - c.y, acc);
+  }
+  __device__ __forceinline__ static float score(float acc, float, float) { return acc; }
+  __device__ __forceinline__ static double seed(double acc, double a, double b, double, double) {
+    const double d = a - b;
+    return fma(d, d, acc);
+  }
+};
+
+template <int PK>
+struct PnormF32 : KeyF32 {
+  using Base = Pnorm<PK, false>;
+  using V = float;
+  using V2 = float2;
+  using VB = float;
+  static constexpr bool kHasB = false;
+  static constexpr bool kCenteredSeed = false;
+  static constexpr bool kCovFilter = false;
+  static constexpr bool kColScale = false;
+  static constexpr int kPairs = kPairsRaw;
+  __device__ __forceinline__ static float step(float acc, float2 r, float2 c, double p) {
+    const float out = fabsf(r.x - c.x);
+    const float in = fabsf(r.y - c.y);
+    if constexpr (PK == 1) return (acc - out) + in;
+    else if constexpr (PK == 3) return fmaf(in * in, in, fmaf(-out * out, out, acc));
+    else if constexpr (PK == 4) { const float o2 = out * out, i2 = in * in; return fmaf(i2, i2, fmaf(-o2, o2, acc)); }
+    else return (acc - powf(out, static_cast<float>(p))) + powf(in, static_cast<float>(p));
+  }
+  __device__ __forceinline__ static float score(float acc, float, float) { return acc; }
+  __device__ __forceinline__ static double seed(double acc, double a, double b, double, double p) {
+    return Pnorm<PK, false>::seed(acc, a, b, 0.0, p);
+  }
+};
+
+template <bool COLSCALE>
+struct ZnormF32 : KeyF32 {
+  using Base = Znorm<COLSCALE>;
+  using V = float;
+  using V2 = float2;
+  using VB = float;
+  static constexpr bool kHasB = true;
+  static constexpr bool kCenteredSeed = true;
+  static constexpr bool kCovFilter = true;
+  static constexpr bool kColScale = COLSCALE;
+  static constexpr int kPairs = kPairsZnorm;
+  __device__ __forceinline__ static float step(float acc, float2 r, float2 c, double) {
+    return fmaf(r.x, c.y, fmaf(c.x, r.y, acc));
+  }
+  __device__ __forceinline__ static float score(float acc, float rb, float cb) {
+    return fmaf(-(acc * cb), rb, 1.0f);
+  }
+  __device__ __forceinline__ static double seed(double acc, double a, double b, double mub, double) {
+    return fma(a, b - mub, acc);
+  }
+};
+
 // ---------------------------------------------------------------------------------------------
-// Tile geometry and shared-memory stage buffers.
+// Tile geometry and shared memory.
 
 template <int D, int T, int S>
 struct Geo {
@@ -222,22 +319,25 @@ struct Geo {
 // operands for stage st+1, so one copy of the K-wide window is resident (not two). Thresholds
 // (4 B per column) are re-read for the whole live window every stage (fresh minima from other
 // CTAs) and double-buffered with the row operands.
-template <bool HASB, int D, int T, int S>
+template <class P, int D, int T, int S>
 struct SweepSmem {
   using G = Geo<D, T, S>;
+  using V2 = typename P::V2;
+  using VB = typename P::VB;
+  static constexpr bool HASB = P::kHasB;
   static_assert(G::RING % D == 0 && S % D == 0, "stage and ring must be multiples of D");
   static constexpr int NCB = G::NCOL / D + 1;  // column blocks of D
-  double2 colA[G::RINGP];                      // ring: A[cbase + X] at pad(X mod RING)
-  double colB[HASB ? G::RINGP : 2];            // ring: B[cbase + 1 + X]
+  V2 colA[G::RINGP];                           // ring: A[cbase + X] at pad(X mod RING)
+  VB colB[HASB ? G::RINGP : 2];                // ring: B[cbase + 1 + X]
   int colT[2][G::NCOLP];                       // hi32(best[i0 + kb + 1 + x].v), exact
   int colBM[2][NCB];                           // max of colT over aligned blocks of D
-  double2 rowA[2][S];                          // A[i0 + x]
-  double rowB[2][HASB ? S : 2];                // B[i0 + 1 + x]
+  V2 rowA[2][S];                               // A[i0 + x]
+  VB rowB[2][HASB ? S : 2];                    // B[i0 + 1 + x]
   int rowT[2][S];                              // hi32(best[i0 + 1 + x].v), exact
   int rowBM[2][S / D];                         // max of rowT over aligned blocks of D
   // z-norm filter scales, rounded DOWN (a smaller scale only loosens the filter): per aligned
-  // block of D columns in a ring of RING/D blocks (filled once, when the block arrives) and per
-  // block of D rows of the stage.
+  // block of D columns in a ring of RING/D blocks (filled once, when the block arrives), per
+  // block of D rows and per row of the stage.
   float colIB[HASB ? G::RING / D : 1];         // <= 1 / max colB of the block
   float rowIB[2][HASB ? S / D : 1];            // <= 1 / max rowB of the block
   float rowIBx[2][HASB ? S : 1];               // <= 1 / rowB of each row
@@ -245,8 +345,10 @@ struct SweepSmem {
 
 struct SweepParams {
   const double* t;        // series, n samples
-  const double2* A;       // per-position operand pairs, valid [0, L-1)
-  const double* B;        // per-position scale (z-norm), valid [0, L)
+  const double2* A;       // FP64 per-position operand pairs, valid [0, L-1)
+  const double* B;        // FP64 per-position scale (z-norm), valid [0, L)
+  const float2* A32;      // FP32 mode operand pairs
+  const float* B32;       // FP32 mode scales
   const double* mu;       // window means (z-norm), valid [0, L)
   BestEntry* best;        // L entries
   const int2* tiles;      // (first diagonal kb, first row ra) per CTA
@@ -257,20 +359,30 @@ struct SweepParams {
   unsigned long long* stats;  // optional diagnostics (MPROF_STATS): [0] replays [1] offers
 };
 
-// ---------------------------------------------------------------------------------------------
-// cp.async helpers (LDGSTS). src_bytes = 0 zero-fills the destination.
+template <class P>
+__device__ __forceinline__ const typename P::V2* pairs_of(const SweepParams& prm) {
+  if constexpr (sizeof(typename P::V) == 8) return prm.A;
+  else return prm.A32;
+}
+template <class P>
+__device__ __forceinline__ const typename P::VB* scales_of(const SweepParams& prm) {
+  if constexpr (sizeof(typename P::V) == 8) return prm.B;
+  else return prm.B32;
+}
 
-__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes_src, int size) {
+// ---------------------------------------------------------------------------------------------
+// cp.async helpers (LDGSTS). An invalid source zero-fills the destination.
+
+template <int SIZE>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  if (size == 16) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
-                 "r"(bytes_src));
-  } else if (size == 8) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
-                 "r"(bytes_src));
+  const int src = valid ? SIZE : 0;
+  if constexpr (SIZE == 16) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+  } else if constexpr (SIZE == 8) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
   } else {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem),
-                 "r"(bytes_src));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
   }
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
@@ -280,24 +392,16 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Exact slow path for one substep of one thread: D cells (target row `row`, columns
-// col0 + d). Cells flagged by the high-word filter (or all valid cells when FORCE) are merged
-// into the global profile: columns individually (distinct per cell), the row through a warp
-// lexicographic reduction and one CAS per warp. Shared thresholds are lowered with atomicMin.
+// Exact slow path.
 
 template <int D>
 struct Cells {
   double v[D];
 };
 
-// Exact slow path for one BLOCK of D sub-steps of ONE lane, called divergently when the block's
-// minimum high word passed the block threshold. The block is REPLAYED from the accumulators saved
-// at its start with the identical arithmetic (bit-identical cell values), and every cell whose
-// high word is <= the current exact column (row) threshold in shared memory (colT / rowT) is
-// merged into the global column (row) minimum; thresholds are lowered with shared atomicMin.
 template <class P, int D>
 struct Acc {
-  double a[D];
+  typename P::V a[D];
 };
 
 // Exact merge of one flagged cell (rarely reached): column entry first, then the row candidate.
@@ -316,22 +420,28 @@ __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhi
   }
 }
 
-// The replay of one block (D sub-steps x D diagonals of one lane), fully unrolled. The 2D-1
-// column operands of the block are two aligned runs of D in the ring (c1 = X0+s+xb, c2 = +D) and
-// the thresholds two aligned runs in the stage buffer; cell (u, d) uses run entry u + d.
+// The replay of one block (D sub-steps x D diagonals of one lane), fully unrolled, from the
+// accumulators saved at the block start: bit-identical recomputation of the fast path, then every
+// cell whose (FP64-promoted) value has a high word <= the current exact column (row) threshold
+// in shared memory is merged. The 2D-1 column operands of the block are two aligned runs of D in
+// the ring (c1 = X0+s+xb, c2 = +D), the thresholds two aligned runs in the stage buffer; cell
+// (u, d) uses run entry u + d.
 template <class P, int D, bool GUARD>
 __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0, int kt, int kend,
-                                          int L, double p, const double2* cA1, const double2* cA2,
-                                          const double* cB1, const double* cB2, int* cT1,
-                                          int* cT2, const double2* rowA, const double* rowB,
+                                          int L, double p, const typename P::V2* cA1,
+                                          const typename P::V2* cA2, const typename P::VB* cB1,
+                                          const typename P::VB* cB2, int* cT1, int* cT2,
+                                          const typename P::V2* rowA, const typename P::VB* rowB,
                                           int* rowT, BestEntry* best, unsigned long long* stats) {
+  using V = typename P::V;
+  using V2 = typename P::V2;
   if (stats) atomicAdd(&stats[0], 1ull);
 #pragma unroll
   for (int u = 0; u < D; ++u) {
     if (GUARD && s + u >= cnt) break;
     const int x = s + u;
-    const double2 r = rowA[x];
-    const double rb = P::kHasB ? rowB[x] : 0.0;
+    const V2 r = rowA[x];
+    const V rb = P::kHasB ? rowB[x] : V(0);
     const int row = i0 + x + 1;
     const int tr = *reinterpret_cast<volatile int*>(&rowT[x]);
     unsigned long long rv = kInfBits;
@@ -339,9 +449,10 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int e = u + d;  // entry of the block's column run
-      const double2 c = e < D ? cA1[e] : cA2[e - D];
+      const V2 c = e < D ? cA1[e] : cA2[e - D];
       acc.a[d] = P::step(acc.a[d], r, c, p);
-      const double v = P::score(acc.a[d], rb, P::kHasB ? (e < D ? cB1[e] : cB2[e - D]) : 0.0);
+      const double v = static_cast<double>(
+          P::score(acc.a[d], rb, P::kHasB ? (e < D ? cB1[e] : cB2[e - D]) : V(0)));
       if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) continue;
       const int h = __double2hiint(v);
       int* ct = e < D ? &cT1[e] : &cT2[e - D];
@@ -390,24 +501,22 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 // ---------------------------------------------------------------------------------------------
 // One stage of S (or cnt < S) row transitions i -> i+1, i in [i0, i0+cnt).
 // Filter: per block of D sub-steps a thread touches D rows and 2D-1 columns; theta = max of
-// their thresholds (three shared loads per block, precomputed block maxima). A cell can only
-// improve (or tie) its row or column minimum if its high word is <= theta. The hot loop only
-// keeps the running minimum high word of the block (a VIMNMX3 tree, no branch); a block that
-// passes is replayed exactly by `replay_block`.
+// their thresholds (block maxima precomputed per stage). A cell can only improve (or tie) its
+// row or column minimum if its key is <= theta. The hot loop keeps the running minimum key of
+// the block (a VIMNMX3 tree, no branch); a block that passes is replayed by `replay_block`.
 
 template <class P, int D, int T, int S, bool GUARD>
-__device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int b, int X0,
-                                          double (&acc)[D], int i0, int cnt, int kt, int kend,
-                                          int L, BestEntry* best, double p,
+__device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int X0,
+                                          typename P::V (&acc)[D], int i0, int cnt, int kt,
+                                          int kend, int L, BestEntry* best, double p,
                                           unsigned long long* stats) {
   using G = Geo<D, T, S>;
-  // z-norm filter form: 0 = covariance only vs a block bound (2 DFMA per cell; loose when the
-  // window scales B vary inside a block, e.g. short windows); 1 = cov * B_j per cell vs a per-row
-  // bound (2 DFMA + 1 DMUL per cell; tight up to the block's max threshold).
+  using V2 = typename P::V2;
+  using VB = typename P::VB;
   constexpr bool kColScale = P::kColScale;
   const int xb = threadIdx.x * D;
-  double2 cA[D];
-  double cB[D];
+  V2 cA[D];
+  VB cB[D];
   {
     const int q0 = G::pad((X0 + xb) % G::RING);  // X0 + xb is a multiple of D: no wrap inside
 #pragma unroll
@@ -416,16 +525,16 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
       if constexpr (kColScale) cB[d] = sm.colB[q0 + d];
     }
   }
-  const double2* rowA = sm.rowA[b];
+  const V2* rowA = sm.rowA[b];
   for (int s = 0; s < cnt; s += D) {
     // the D operands entering during this block are contiguous in the ring: constant offsets
     const int qn = G::pad((X0 + s + xb + D) % G::RING);
-    const double2* nA = &sm.colA[qn];
-    const double* nB = &sm.colB[P::kHasB ? qn : 0];
+    const V2* nA = &sm.colA[qn];
+    const VB* nB = &sm.colB[P::kHasB ? qn : 0];
     const int cb = s / D + threadIdx.x;
     const int tmax = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
-    int theta = tmax;
-    double num = 0.0;  // kColScale: 1 - tau_max (with margin), 0 = every cell may qualify
+    int theta = P::tau(tmax);
+    double num = 0.0;  // covariance filters: 1 - tau_max (with margin), 0 = every cell may pass
     if constexpr (P::kCovFilter) {
       if (tmax >= 0x3FF00000) {
         theta = INT_MAX;  // some threshold >= 1: any cell may qualify
@@ -434,8 +543,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
         if constexpr (!kColScale) {
           const int cq = (X0 / D + cb) % (G::RING / D);
           const float ic = fminf(sm.colIB[cq], sm.colIB[cq + 1 == G::RING / D ? 0 : cq + 1]);
-          const double th = num * static_cast<double>(sm.rowIB[b][s / D]) * static_cast<double>(ic);
-          theta = ~__double2hiint(th);
+          theta = P::cov_bound(num * static_cast<double>(sm.rowIB[b][s / D]) * static_cast<double>(ic));
         }
       }
     }
@@ -448,7 +556,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
     for (int u = 0; u < D; ++u) {
       if (GUARD && s + u >= cnt) break;
       const int x = s + u;
-      const double2 r = rowA[x];
+      const V2 r = rowA[x];
       const int row = i0 + x + 1;
       int hu = INT_MAX;
 #pragma unroll
@@ -456,7 +564,8 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
         const int sl = (d + u) % D;
         acc[d] = P::step(acc[d], r, cA[sl], p);
         int h;
-        if constexpr (kColScale) h = ~__double2hiint(acc[d] * cB[sl]);
+        if constexpr (kColScale) h = P::cov_key(acc[d] * cB[sl]);
+        else if constexpr (P::kCovFilter) h = P::cov_key(acc[d]);
         else h = P::key(acc[d]);
         if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
         hu = min(hu, h);
@@ -464,7 +573,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
       if constexpr (kColScale) {
         // row bound for this sub-step: cov * B_j >= (1 - tau) / B_i
         const int tu = (num == 0.0) ? INT_MAX
-                                    : ~__double2hiint(num * static_cast<double>(sm.rowIBx[b][x]));
+                                    : P::cov_bound(num * static_cast<double>(sm.rowIBx[b][x]));
         hit |= hu <= tu;
       } else {
         hmin = min(hmin, hu);
@@ -486,11 +595,25 @@ __device__ __forceinline__ void run_stage(SweepSmem<P::kHasB, D, T, S>& sm, int 
   }
 }
 
+// Upper bound of B from its storage word: FP64 high word (low word all ones), FP32 bits.
+template <class VB>
+__device__ __forceinline__ int scale_word(const VB* p) {
+  if constexpr (sizeof(VB) == 8) return reinterpret_cast<const int*>(p)[1];
+  else return __float_as_int(*p);
+}
+// B >= 0: a lower bound of 1 / max B from the largest word of a block.
+template <class VB>
+__device__ __forceinline__ float inv_bound(int w) {
+  if constexpr (sizeof(VB) == 8) return __frcp_rd(__double2float_ru(__hiloint2double(w, -1)));
+  else return __frcp_rd(__int_as_float(w));
+}
+
 // Block maxima of the freshly loaded thresholds (after the stage's cp.async completed).
-template <bool HASB, int D, int T, int S>
-__device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, int b, int X0) {
+template <class P, int D, int T, int S>
+__device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b, int X0) {
   using G = Geo<D, T, S>;
-  using SM = SweepSmem<HASB, D, T, S>;
+  using SM = SweepSmem<P, D, T, S>;
+  using VB = typename P::VB;
   for (int blk = threadIdx.x; blk < SM::NCB; blk += T) {
     int mx = INT_MIN;
 #pragma unroll
@@ -506,30 +629,23 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, in
     for (int d = 0; d < D; ++d) mx = max(mx, sm.rowT[b][blk * D + d]);
     sm.rowBM[b][blk] = mx;
   }
-  if constexpr (HASB) {
-    // B >= 0: the maximum high word bounds max B from above (low word all ones); its float,
-    // rounded up, and the reciprocal rounded down give a lower bound of 1 / max B.
-    auto inv_bound = [](int hmax) -> float {
-      return __frcp_rd(__double2float_ru(__hiloint2double(hmax, -1)));
-    };
+  if constexpr (P::kHasB) {
     const int first = (X0 == 0) ? 0 : (X0 + G::K) / D;  // column blocks that arrived for this stage
     const int last = (X0 + G::NCOL) / D;
     for (int bx = first + static_cast<int>(threadIdx.x); bx < last; bx += T) {
       const int q = G::pad((bx * D) % G::RING);
-      const int* w = reinterpret_cast<const int*>(&sm.colB[q]);
       int hmax = 0;
 #pragma unroll
-      for (int d = 0; d < D; ++d) hmax = max(hmax, w[2 * d + 1]);
-      sm.colIB[bx % (G::RING / D)] = inv_bound(hmax);
+      for (int d = 0; d < D; ++d) hmax = max(hmax, scale_word<VB>(&sm.colB[q + d]));
+      sm.colIB[bx % (G::RING / D)] = inv_bound<VB>(hmax);
     }
     for (int x = threadIdx.x; x < S; x += T)
-      sm.rowIBx[b][x] = inv_bound(reinterpret_cast<const int*>(&sm.rowB[b][x])[1]);
+      sm.rowIBx[b][x] = inv_bound<VB>(scale_word<VB>(&sm.rowB[b][x]));
     for (int blk = threadIdx.x; blk < S / D; blk += T) {
-      const int* w = reinterpret_cast<const int*>(&sm.rowB[b][blk * D]);
       int hmax = 0;
 #pragma unroll
-      for (int d = 0; d < D; ++d) hmax = max(hmax, w[2 * d + 1]);
-      sm.rowIB[b][blk] = inv_bound(hmax);
+      for (int d = 0; d < D; ++d) hmax = max(hmax, scale_word<VB>(&sm.rowB[b][blk * D + d]));
+      sm.rowIB[b][blk] = inv_bound<VB>(hmax);
     }
   }
 }
@@ -537,10 +653,14 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<HASB, D, T, S>& sm, in
 // Issue the cp.async copies of stage st (row transitions i0 .. i0+S-1, i0 = ra + st*S):
 // its row operands and thresholds, the thresholds of its whole live column window, and the
 // column operands that enter the ring with it (all NCOL for stage 0, S afterwards).
-template <bool HASB, int D, int T, int S>
-__device__ __forceinline__ void load_stage(SweepSmem<HASB, D, T, S>& sm, const SweepParams& prm,
+template <class P, int D, int T, int S>
+__device__ __forceinline__ void load_stage(SweepSmem<P, D, T, S>& sm, const SweepParams& prm,
                                            int st, int ra, int kb) {
   using G = Geo<D, T, S>;
+  using V2 = typename P::V2;
+  using VB = typename P::VB;
+  const V2* A = pairs_of<P>(prm);
+  const VB* Bs = scales_of<P>(prm);
   const int L = prm.L;
   const int b = st & 1;
   const int i0 = ra + st * S;
@@ -548,7 +668,7 @@ __device__ __forceinline__ void load_stage(SweepSmem<HASB, D, T, S>& sm, const S
   for (int x = threadIdx.x; x < G::NCOL; x += T) {
     const int pb = i0 + kb + 1 + x;
     const bool vb = pb < L;
-    cp_async(&sm.colT[b][G::pad(x)], bestw + 4 * (vb ? pb : 0) + 1, vb ? 4 : 0, 4);
+    cp_async<4>(&sm.colT[b][G::pad(x)], bestw + 4 * (vb ? pb : 0) + 1, vb);
   }
   const int Xlo = st == 0 ? 0 : st * S + G::K;
   const int Xhi = st * S + G::NCOL;
@@ -556,16 +676,16 @@ __device__ __forceinline__ void load_stage(SweepSmem<HASB, D, T, S>& sm, const S
     const int pa = ra + kb + X;
     const bool va = pa < L - 1, vb = pa + 1 < L;
     const int q = G::pad(X % G::RING);
-    cp_async(&sm.colA[q], prm.A + (va ? pa : 0), va ? 16 : 0, 16);
-    if constexpr (HASB) cp_async(&sm.colB[q], prm.B + (vb ? pa + 1 : 0), vb ? 8 : 0, 8);
+    cp_async<sizeof(V2)>(&sm.colA[q], A + (va ? pa : 0), va);
+    if constexpr (P::kHasB) cp_async<sizeof(VB)>(&sm.colB[q], Bs + (vb ? pa + 1 : 0), vb);
   }
   for (int x = threadIdx.x; x < S; x += T) {
     const int pa = i0 + x;
     const int pb = pa + 1;
     const bool va = pa < L - 1, vb = pb < L;
-    cp_async(&sm.rowA[b][x], prm.A + (va ? pa : 0), va ? 16 : 0, 16);
-    if constexpr (HASB) cp_async(&sm.rowB[b][x], prm.B + (vb ? pb : 0), vb ? 8 : 0, 8);
-    cp_async(&sm.rowT[b][x], bestw + 4 * (vb ? pb : 0) + 1, vb ? 4 : 0, 4);
+    cp_async<sizeof(V2)>(&sm.rowA[b][x], A + (va ? pa : 0), va);
+    if constexpr (P::kHasB) cp_async<sizeof(VB)>(&sm.rowB[b][x], Bs + (vb ? pb : 0), vb);
+    cp_async<4>(&sm.rowT[b][x], bestw + 4 * (vb ? pb : 0) + 1, vb);
   }
 }
 
@@ -575,7 +695,9 @@ __device__ __forceinline__ void load_stage(SweepSmem<HASB, D, T, S>& sm, const S
 template <class P, int D, int T, int S, int MINB>
 __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   using G = Geo<D, T, S>;
-  using SM = SweepSmem<P::kHasB, D, T, S>;
+  using SM = SweepSmem<P, D, T, S>;
+  using V = typename P::V;
+  using VB = typename P::VB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -587,12 +709,12 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   const int kend = min(kb + G::K, prm.k_hi);
   const int re = min(ra + prm.R, L - kb);  // exclusive row end of the tile
 
-  // ---- seed: acc[d] = direct length-m sum for the pair (ra, ra + kt + d) ----------------
-  double acc[D];
+  // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d) --------------------
+  double sacc[D];
   double muc[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    acc[d] = 0.0;
+    sacc[d] = 0.0;
     muc[d] = 0.0;
     if constexpr (P::kCenteredSeed) {
       const int j = ra + kt + d;
@@ -629,24 +751,28 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
           if (l + u >= cnt) break;
           const double a = srow[l + u];
 #pragma unroll
-          for (int d = 0; d < D; ++d) acc[d] = P::seed(acc[d], a, w[(d + u) % D], muc[d], prm.p);
+          for (int d = 0; d < D; ++d) sacc[d] = P::seed(sacc[d], a, w[(d + u) % D], muc[d], prm.p);
           w[u] = scol[G::pad(l + u + xb + D)];
         }
       }
     }
   }
+  V acc[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) acc[d] = static_cast<V>(sacc[d]);
 
   // ---- the seed cells (ra, ra + k): exact merge -------------------------------------------
   {
+    const VB* Bs = scales_of<P>(prm);
     Cells<D> c;
     unsigned valid = 0;
-    const double rb = P::kHasB ? prm.B[ra] : 0.0;
+    const VB rb = P::kHasB ? Bs[ra] : VB(0);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int k = kt + d;
       const bool ok = (k < kend) && (ra + k <= L - 1);
-      const double cb = (P::kHasB && ok) ? prm.B[ra + k] : 0.0;
-      c.v[d] = P::score(acc[d], rb, cb);
+      const VB cb = (P::kHasB && ok) ? Bs[ra + k] : VB(0);
+      c.v[d] = static_cast<double>(P::score(acc[d], rb, cb));
       valid |= (ok ? 1u : 0u) << d;
     }
     resolve_seed<D>(c, valid, ra, ra + kt, prm.best);
@@ -656,16 +782,16 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   const int steps = re - 1 - ra;
   if (steps <= 0) return;
   __syncthreads();  // seed scratch reuse
-  load_stage<P::kHasB, D, T, S>(sm, prm, 0, ra, kb);
+  load_stage<P, D, T, S>(sm, prm, 0, ra, kb);
   cp_async_commit();
   for (int st = 0, s0 = 0; s0 < steps; s0 += S, ++st) {
     const int cnt = min(S, steps - s0);
     const int i0 = ra + s0;
-    if (s0 + S < steps) load_stage<P::kHasB, D, T, S>(sm, prm, st + 1, ra, kb);
+    if (s0 + S < steps) load_stage<P, D, T, S>(sm, prm, st + 1, ra, kb);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    stage_block_max<P::kHasB, D, T, S>(sm, st & 1, s0);
+    stage_block_max<P, D, T, S>(sm, st & 1, s0);
     __syncthreads();
     const bool full = (cnt == S) && (kb + G::K <= prm.k_hi) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {

@@ -16,12 +16,15 @@ fn = {"e": mp.aamp, "p": mp.aamp_pnorm, "z": mp.acamp}[fam]
 ctx = mp.Context(0)
 ctx.set_timing(True)
 cfg = mp.ProfileConfig(m, kind)
+import os  # noqa: E402
+if os.environ.get("MPROF_PRECISION") == "fp32":
+    cfg.precision = mp.Precision.FP32
 ts = mp.make_time_series(t)
 ms = []
 for r in range(4):
     res = fn(ts, cfg, ctx=ctx)
     ms.append(res.info.sweep_ms)
 b = min(ms[1:])
-print(json.dumps({"gen": gen, "n": n, "m": m, "fam": fam, "sweep_ms": round(b, 3),
+print(json.dumps({"prec": os.environ.get("MPROF_PRECISION", "fp64"), "gen": gen, "n": n, "m": m, "fam": fam, "sweep_ms": round(b, 3),
                   "cells_per_s": f"{res.info.cells / (b * 1e-3):.3e}", "tiles": res.info.tiles,
                   "R": res.info.rows_per_tile}))
