@@ -514,12 +514,19 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, long long R, long l
   return MPROF_OK;
 }
 
+// __launch_bounds__ minimum CTAs per SM: the policy's own choice if it has one, else the build's.
+template <class P>
+constexpr int min_blocks() {
+  if constexpr (requires { P::kMinBlocks; }) return P::kMinBlocks;
+  else return MPROF_MIN_BLOCKS;
+}
+
 template <class P>
 int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int k1,
                      bool first_diag, uint32_t* launches, float* ms) {
   using SM = SweepSmem<P, kD, kT, kS>;
   const size_t smem = sizeof(SM);
-  auto kern = sweep_kernel<P, kD, kT, kS, MPROF_MIN_BLOCKS>;
+  auto kern = sweep_kernel<P, kD, kT, kS, min_blocks<P>()>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (first_diag && k1 <= prm.L - 1) {
     k_first_diag<P><<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);

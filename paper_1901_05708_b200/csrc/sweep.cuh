@@ -214,6 +214,7 @@ struct Znorm : KeyF64 {
   static constexpr bool kCenteredSeed = true;
   static constexpr bool kCovFilter = true;
   static constexpr bool kColScale = COLSCALE;
+  static constexpr int kMinBlocks = COLSCALE ? 3 : 4;  // measured: the +cB ring wants registers
   static constexpr int kPairs = kPairsZnorm;
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     return fma(r.x, c.y, fma(c.x, r.y, acc));
@@ -779,27 +780,39 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   }
 
   // ---- stage pipeline over the row transitions ra .. re-2 ---------------------------------
+  // Two CTA barriers per stage: (1) stage st+1's copies landed and every warp finished stage st
+  // (its row/threshold buffers and the ring slots of offsets [st*S, st*S + S) are free), then
+  // the block maxima of st+1 are computed and the copies of st+2 are issued into the freed
+  // buffers, a whole stage ahead of use; (2) the block maxima are visible.
   const int steps = re - 1 - ra;
   if (steps <= 0) return;
+  const int nst = (steps + S - 1) / S;
   __syncthreads();  // seed scratch reuse
   load_stage<P, D, T, S>(sm, prm, 0, ra, kb);
   cp_async_commit();
-  for (int st = 0, s0 = 0; s0 < steps; s0 += S, ++st) {
+  cp_async_wait<0>();
+  __syncthreads();
+  stage_block_max<P, D, T, S>(sm, 0, 0);
+  if (nst > 1) load_stage<P, D, T, S>(sm, prm, 1, ra, kb);
+  cp_async_commit();
+  __syncthreads();
+  for (int st = 0; st < nst; ++st) {
+    const int s0 = st * S;
     const int cnt = min(S, steps - s0);
     const int i0 = ra + s0;
-    if (s0 + S < steps) load_stage<P, D, T, S>(sm, prm, st + 1, ra, kb);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    stage_block_max<P, D, T, S>(sm, st & 1, s0);
-    __syncthreads();
     const bool full = (cnt == S) && (kb + G::K <= prm.k_hi) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {
       run_stage<P, D, T, S, false>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     } else {
       run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     }
-    __syncthreads();  // stage st's buffers (rows, thresholds, ring slots) are free for st+2
+    if (st + 1 == nst) break;
+    cp_async_wait<0>();
+    __syncthreads();
+    stage_block_max<P, D, T, S>(sm, (st + 1) & 1, s0 + S);
+    if (st + 2 < nst) load_stage<P, D, T, S>(sm, prm, st + 2, ra, kb);
+    cp_async_commit();
+    __syncthreads();
   }
 }
 
