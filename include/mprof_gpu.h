@@ -158,6 +158,27 @@ int32_t mprof_finalize_device(mprof_ctx* ctx, const double* d_t, uint64_t n, con
 int32_t mprof_merge_device(mprof_ctx* ctx, double* d_cmp, int64_t* d_idx,
                            const double* d_other_cmp, const int64_t* d_other_idx, uint64_t L);
 
+/* ---- streaming extension: EngineState ---------------------------------------------------- */
+/* build_engine_state / extend_profile (/root/reference/proj/include/mprof/engine_state.hpp:26-52,
+ * /root/reference/proj/src/engine_state.cpp:11-156). The state keeps the series and the
+ * comparison-space profile on the device. extend sweeps ONLY the cells that involve an appended
+ * window — on the time-reversed series those are rows [0, dL) of every diagonal — and merges
+ * them into the stored profile; the result equals a from-scratch profile of the extended series
+ * (parity tolerance; the reference's bit-exact cursor replay is CPU arithmetic). */
+typedef struct mprof_state mprof_state;
+int32_t mprof_state_build(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                          mprof_state** out, mprof_run_info* info);
+/* NonFinite for a bad sample (nothing changes); count == 0 leaves the state unchanged. */
+int32_t mprof_state_extend(mprof_state* st, const double* samples, uint64_t count,
+                           mprof_run_info* info);
+int32_t mprof_state_clone(const mprof_state* st, mprof_state** out);
+uint64_t mprof_state_series_length(const mprof_state* st);
+/* P, I (and optionally cmp) of length n - m + 1 to host buffers; any pointer may be NULL. */
+int32_t mprof_state_profile(mprof_state* st, double* P, int64_t* I, double* cmp);
+/* The state's series (n samples) to a host buffer. */
+int32_t mprof_state_series(const mprof_state* st, double* t);
+void mprof_state_destroy(mprof_state* st);
+
 /* ---- multi-GPU partition (host-side math, no device needed) ------------------------------ */
 /* Equal-area cut of the diagonal range [exclusion, n-m] into `parts` contiguous bands; writes
  * parts+1 boundaries (cuts[0] = exclusion, cuts[parts] = n-m+1). Area(k) = L - k cells. */

@@ -30,7 +30,8 @@ __all__ = [
     "Precision", "ProfileConfig", "TimeSeries", "make_time_series", "validate_config",
     "profile_length", "default_flat_threshold", "MatrixProfile", "RunInfo", "aamp",
     "aamp_pnorm", "acamp", "sweep_device", "finalize_device", "merge_device", "band_cuts",
-    "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context",
+    "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context", "EngineState",
+    "build_engine_state", "extend_profile",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libmprof_gpu.so"
@@ -245,6 +246,14 @@ EXPORTS = {
                                     C.POINTER(C.c_uint64)]),
     "mprof_band_cells": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),
     "mprof_fp64_peak": (C.c_int32, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
+    "mprof_state_build": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                      C.POINTER(C.c_void_p), C.POINTER(RunInfo)]),
+    "mprof_state_extend": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(RunInfo)]),
+    "mprof_state_clone": (C.c_int32, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mprof_state_series_length": (C.c_uint64, [C.c_void_p]),
+    "mprof_state_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mprof_state_series": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "mprof_state_destroy": (None, [C.c_void_p]),
 }
 
 _lib = None
@@ -418,3 +427,88 @@ def fp64_peak(ctx: Optional[Context] = None) -> tuple:
     ms = C.c_float()
     _raise(lib().mprof_fp64_peak(_ctx_handle(ctx), C.byref(g), C.byref(ms)))
     return float(g.value), float(ms.value)
+
+
+# --------------------------------------------------------------------------------------------
+# streaming extension: mprof::EngineState / build_engine_state / extend_profile
+# (/root/reference/proj/include/mprof/engine_state.hpp:26-52)
+
+class EngineState:
+    """A computed profile plus what is needed to grow it: here the series and the
+    comparison-space profile held on the GPU (the reference keeps per-diagonal tail cursors;
+    the GPU re-derives the new cells from the series instead)."""
+
+    def __init__(self, handle, cfg: ProfileConfig, info: Optional[RunInfo] = None):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self.cfg = cfg
+        self.info = info
+        self._cache = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            if self._h:
+                lib().mprof_state_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def _load(self):
+        if self._cache is None:
+            n = int(lib().mprof_state_series_length(self._h))
+            L = n - self.cfg.m + 1
+            t = np.empty(n)
+            P = np.empty(L)
+            I = np.empty(L, dtype=np.int64)
+            cmp = np.empty(L)
+            _raise(lib().mprof_state_series(self._h, t.ctypes.data))
+            _raise(lib().mprof_state_profile(self._h, P.ctypes.data, I.ctypes.data, cmp.ctypes.data))
+            self._cache = (t, MatrixProfile(P, I, self.cfg.m, self.cfg.kind, self.info), cmp)
+        return self._cache
+
+    @property
+    def ts(self) -> TimeSeries:
+        return make_time_series(self._load()[0])
+
+    @property
+    def profile(self) -> MatrixProfile:
+        return self._load()[1]
+
+    @property
+    def comparison(self) -> np.ndarray:
+        return self._load()[2]
+
+    def complete(self) -> bool:
+        # the GPU sweep cannot be cancelled mid-way: every diagonal always completes
+        return True
+
+
+def build_engine_state(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Callable] = None,
+                       threads: int = 0, ctx: Optional[Context] = None) -> EngineState:
+    """engine_state.hpp:44-45 (any distance family)."""
+    _check_int_fields(cfg)
+    v = ts.values()
+    h = C.c_void_p()
+    info = RunInfo()
+    c = _to_c(cfg)
+    _raise(lib().mprof_state_build(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
+                                   C.byref(h), C.byref(info)))
+    if progress is not None:
+        progress(int(info.diagonals), int(info.diagonals))
+    return EngineState(h, cfg.copy(), info)
+
+
+def extend_profile(state: EngineState, new_samples: Sequence[float]) -> EngineState:
+    """engine_state.hpp:52: a NEW state for the extended series (the input is unchanged).
+    NonFinite for a bad sample; an empty span returns an equal state."""
+    s = np.ascontiguousarray(np.asarray(new_samples, dtype=np.float64).reshape(-1))
+    bad = np.flatnonzero(~np.isfinite(s))
+    if bad.size:
+        raise Error(ErrorCode.NonFinite, f"appended sample {int(bad[0])} is not finite")
+    h = C.c_void_p()
+    _raise(lib().mprof_state_clone(state._h, C.byref(h)))
+    out = EngineState(h, state.cfg.copy())
+    info = RunInfo()
+    _raise(lib().mprof_state_extend(out._h, s.ctypes.data if s.size else None, s.shape[0],
+                                    C.byref(info)))
+    out.info = info
+    return out

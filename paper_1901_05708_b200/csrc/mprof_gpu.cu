@@ -180,7 +180,7 @@ template <class PP>
 __global__ void k_first_diag(SweepParams prm, int k1) {
   using P = typename PP::Base;  // FP64 evaluation, also in FP32 mode
   const int L = prm.L;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + k1 <= L - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + k1 <= L - 1 && i < prm.row_hi;
        i += gridDim.x * blockDim.x) {
     const int j = i + k1;
     const double mui = P::kCenteredSeed ? prm.mu[i] : 0.0;
@@ -190,8 +190,8 @@ __global__ void k_first_diag(SweepParams prm, int k1) {
     const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
     const unsigned long long vb =
         (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
-    offer(prm.best, i, vb, j);
-    offer(prm.best, j, vb, i);
+    offer(prm.best, i, vb, out_index(j, prm.rl));
+    offer(prm.best, j, vb, out_index(i, prm.rl));
   }
 }
 
@@ -253,6 +253,37 @@ __global__ void k_flat_fix(const double* __restrict__ B, int L, int k_lo, int k_
     const unsigned long long one = static_cast<unsigned long long>(__double_as_longlong(1.0));
     best[i] = (j == INT_MAX) ? BestEntry{kInfBits, kNoIdx} : BestEntry{one, static_cast<long long>(j)};
   }
+}
+
+// ---- streaming extension (build_engine_state / extend_profile) -----------------------------
+__global__ void k_reverse(const double* __restrict__ in, double* __restrict__ out, int n) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    out[p] = in[n - 1 - p];
+}
+
+// Profile of the reversed extended series before the sweep of the new cells: reversed position
+// x' holds original window L_new-1-x'. The dL new windows (x' < dL) start empty; old windows
+// carry their (comparison value, original index) entry; flat windows are pinned (k_init_best).
+__global__ void k_init_from_prev(BestEntry* __restrict__ best, const double* __restrict__ B,
+                                 const double* __restrict__ cmp_old,
+                                 const int64_t* __restrict__ idx_old, int L_old, int L_new) {
+  const int dL = L_new - L_old;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < L_new; x += gridDim.x * blockDim.x) {
+    BestEntry e{kInfBits, kNoIdx};
+    if (B && B[x] == 0.0) {
+      e = BestEntry{0ull, -1};
+    } else if (x >= dL) {
+      const int o = L_new - 1 - x;
+      const long long j = idx_old[o];
+      if (j >= 0) e = BestEntry{static_cast<unsigned long long>(__double_as_longlong(cmp_old[o])), j};
+    }
+    best[x] = e;
+  }
+}
+
+__global__ void k_unreverse(const BestEntry* __restrict__ in, BestEntry* __restrict__ out, int L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
+    out[i] = in[L - 1 - i];
 }
 
 __global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__ cmp,
@@ -385,6 +416,25 @@ struct mprof_ctx {
   double* d_spread = nullptr;
 };
 
+// Device-resident EngineState: the series, the comparison-space profile and scratch.
+struct mprof_state {
+  mprof_ctx* ctx = nullptr;
+  mprof_config cfg;
+  uint64_t n = 0;
+  double* t = nullptr;       // series (device)
+  size_t t_bytes = 0;
+  double* cmp = nullptr;     // comparison values [L]
+  size_t cmp_bytes = 0;
+  int64_t* idx = nullptr;    // neighbours [L]
+  size_t idx_bytes = 0;
+  double* rev = nullptr;     // reversed series scratch
+  size_t rev_bytes = 0;
+  void* fwd = nullptr;       // BestEntry scratch [L]
+  size_t fwd_bytes = 0;
+  double* P = nullptr;       // finalized distances scratch [L]
+  size_t P_bytes = 0;
+};
+
 namespace {
 
 int32_t ensure(void** p, size_t* have, size_t need) {
@@ -473,13 +523,15 @@ int32_t ensure_znorm_stats(mprof_ctx* c, const double* d_t, uint64_t n, const mp
 // rows-per-tile choice: exact mode aligns runs to refresh_interval (bit-exact reseeding points,
 // diag_scan.hpp:97-104) or runs whole diagonals; the fast mode balances seeding cost (m/(2R) of
 // the cell work) against having enough tiles for every SM.
-long long count_tiles(int L, int k_lo, int k_hi, long long R) {
+// Rows of diagonal block kb that hold cells: [0, min(L - kb, row_hi)).
+long long count_tiles(int L, int k_lo, int k_hi, int row_hi, long long R) {
   long long t = 0;
-  for (long long kb = k_lo; kb < k_hi; kb += kK) t += (L - kb + R - 1) / R;
+  for (long long kb = k_lo; kb < k_hi; kb += kK)
+    t += (std::min<long long>(L - kb, row_hi) + R - 1) / R;
   return t;
 }
 
-long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int num_sms) {
+long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int num_sms) {
   if (cfg->exact) {
     if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
     return L;  // the whole diagonal is one run, like the reference's refresh = 0
@@ -487,21 +539,24 @@ long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int num_s
   long long R = std::max<long long>(32LL * (long long)cfg->m, 8LL * kS);
   R = (R + kS - 1) / kS * kS;
   const long long want = 16LL * num_sms;
-  while (R > 2 * kS && count_tiles(L, k_lo, k_hi, R) < want) R = std::max<long long>(2 * kS, (R / 2 + kS - 1) / kS * kS);
+  while (R > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, R) < want)
+    R = std::max<long long>(2 * kS, (R / 2 + kS - 1) / kS * kS);
   if (const char* e = getenv("MPROF_ROWS_PER_TILE")) R = std::max(1LL, atoll(e));  // experiments
   if (cfg->refresh_interval > 0) R = std::min<long long>(R, (long long)cfg->refresh_interval);
   return R;
 }
 
-int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, long long R, long long* ntiles) {
-  const long long key[6] = {L, k_lo, k_hi, R, kK, 1};
+int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long long R,
+                    long long* ntiles) {
+  const long long key[6] = {L, k_lo, k_hi, R, kK, row_hi};
   if (std::equal(key, key + 6, c->tiles_key)) {
     *ntiles = (long long)c->tiles_h.size();
     return MPROF_OK;
   }
   c->tiles_h.clear();
   for (long long kb = k_lo; kb < k_hi; kb += kK)
-    for (long long ra = 0; ra < L - kb; ra += R) c->tiles_h.push_back(make_int2((int)kb, (int)ra));
+    for (long long ra = 0; ra < std::min<long long>(L - kb, row_hi); ra += R)
+      c->tiles_h.push_back(make_int2((int)kb, (int)ra));
   const size_t need = c->tiles_h.size() * sizeof(int2);
   void* p = c->tiles_d;
   int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
@@ -609,6 +664,151 @@ int32_t check_series(const double* t, uint64_t n) {
   return MPROF_OK;
 }
 
+// ---- sweep phases ---------------------------------------------------------------------------
+// (1) operands of series d_t: z-norm statistics, operand pairs (FP64 and FP32), filter form
+int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
+                         const Workspace& w, uint32_t* launches) {
+  const int m = (int)cfg->m;
+  const int L = n - m + 1;
+  const int g = grid_for(L);
+  int32_t st = MPROF_OK;
+  const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  if (zn) {
+    c->stats_t = nullptr;  // force: the series bytes behind d_t may have changed
+    st = ensure_znorm_stats(c, d_t, (uint64_t)n, cfg, w);
+    if (st != MPROF_OK) return st;
+    k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
+    *launches += 2;
+    // filter form for this series: MPROF_ZN_FILTER=cov|col overrides the measured choice
+    const char* force = getenv("MPROF_ZN_FILTER");
+    if (force && !strcmp(force, "cov")) {
+      c->zn_colscale = false;
+    } else if (force && !strcmp(force, "col")) {
+      c->zn_colscale = true;
+    } else {
+      if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
+      CK(cudaMemsetAsync(c->d_spread, 0, 2 * sizeof(double), c->stream));
+      k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.B, L, c->d_spread);
+      double h[2];
+      CK(cudaMemcpyAsync(h, c->d_spread, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      ++*launches;
+      c->zn_colscale = !(h[1] > 0.0 && h[0] / h[1] >= kZnCovFilterMinSpread);
+    }
+  } else {
+    // the fast Euclidean policy slides (delta, sigma) pairs; everything else the raw pairs
+    const bool ds = !cfg->exact && (cfg->family == MPROF_EUCLIDEAN ||
+                                    (cfg->family == MPROF_PNORM && cfg->p == 2.0));
+    k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m, ds ? kPairsDeltaSum : kPairsRaw);
+    ++*launches;
+  }
+  if (cfg->precision == MPROF_FP32) {
+    if (zn) {
+      k_znorm_pairs32<<<g, 256, 0, c->stream>>>(w.A, w.B, w.A32, w.B32, L);
+      ++*launches;
+    } else {
+      CK(cudaMemsetAsync(w.scalars, 0, sizeof(double), c->stream));
+      k_mean<<<grid_for(n), 256, 0, c->stream>>>(d_t, n, w.scalars);
+      const bool ds32 = cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0;
+      k_build_pairs32<<<g, 256, 0, c->stream>>>(d_t, w.A32, L, m, ds32 ? kPairsDeltaSum : kPairsRaw,
+                                                w.scalars);
+      *launches += 2;
+    }
+  }
+  CK(cudaGetLastError());
+  return MPROF_OK;
+}
+
+// (2) the tiles of diagonals [k_lo, k_hi) x rows [0, row_hi) into w.best (initialised by the
+// caller); rl > 0: reflected sweep (indices stored as rl - 1 - idx)
+struct SweepOut {
+  float ms = 0.f;
+  long long ntiles = 0, R = 0;
+};
+
+int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
+                    const Workspace& w, int k_lo, int k_hi, int row_hi, int rl, uint32_t* launches,
+                    SweepOut* out) {
+  const int m = (int)cfg->m;
+  const int L = n - m + 1;
+  if (k_lo >= k_hi || row_hi <= 0) return MPROF_OK;
+  out->R = choose_R(cfg, L, k_lo, k_hi, row_hi, c->num_sms);
+  int32_t st = build_tiles(c, L, k_lo, k_hi, row_hi, out->R, &out->ntiles);
+  if (st != MPROF_OK) return st;
+  SweepParams prm;
+  prm.t = d_t;
+  prm.A = w.A;
+  prm.B = w.B;
+  prm.A32 = w.A32;
+  prm.B32 = w.B32;
+  prm.mu = w.mu;
+  prm.best = w.best;
+  prm.tiles = c->tiles_d;
+  prm.n = n;
+  prm.m = m;
+  prm.L = L;
+  prm.k_hi = k_hi;
+  prm.R = (int)std::min<long long>(out->R, INT_MAX);
+  prm.row_hi = row_hi;
+  prm.rl = rl;
+  prm.p = cfg->p;
+  prm.stats = nullptr;
+  const bool want_stats = getenv("MPROF_STATS") != nullptr;
+  if (want_stats) {
+    CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
+  }
+  st = dispatch_sweep(c, cfg, prm, out->ntiles, k_lo, launches, &out->ms);
+  if (st != MPROF_OK) return st;
+  if (want_stats) {
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, prm.stats, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFreeAsync(prm.stats, c->stream);
+    fprintf(stderr, "[mprof stats] family %d L %d tiles %lld R %lld: replays %llu offers %llu\n",
+            cfg->family, L, out->ntiles, out->R, h[0], h[1]);
+  }
+  return MPROF_OK;
+}
+
+// (3) z-norm flat windows of the band (original coordinates): final entries
+int32_t flat_fix(mprof_ctx* c, const double* B, int L, int k_lo, int k_hi, const Workspace& w,
+                 BestEntry* best, uint32_t* launches) {
+  if (k_lo >= k_hi) return MPROF_OK;
+  const int nch = (L + kChunk - 1) / kChunk;
+  k_flat_chunk_min<<<nch, 256, 0, c->stream>>>(B, L, w.cmin);
+  k_flat_fix<<<grid_for(L), 256, 0, c->stream>>>(B, L, k_lo, k_hi, w.cmin, best);
+  *launches += 2;
+  CK(cudaGetLastError());
+  return MPROF_OK;
+}
+
+void fill_info(mprof_ctx* c, const mprof_config* cfg, uint64_t cells, long long diagonals,
+               const SweepOut& so, uint32_t launches, mprof_run_info* info) {
+  if (!info) return;
+  // FP64-pipe instructions per cell of the hot loop (SASS-audited)
+  float ops = 4.f;
+  if (cfg->family == MPROF_ZNORMALIZED) ops = c->zn_colscale ? 3.125f : 2.f;
+  else if (cfg->exact) ops = (cfg->family == MPROF_PNORM && cfg->p != 1.0 && cfg->p != 2.0) ? 8.f : 6.f;
+  else if (cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0) ops = 3.f;
+  else if (cfg->p == 1.0) ops = 4.f;
+  else if (cfg->p == 3.0 || cfg->p == 4.0) ops = 6.f;
+  else ops = 0.f;  // generic pow: library call, not a fixed count
+  if (cfg->precision == MPROF_FP32) {
+    info->fp64_ops_per_cell = 0.f;
+    info->fp32_ops_per_cell = ops;
+  } else {
+    info->fp64_ops_per_cell = ops;
+    info->fp32_ops_per_cell = 0.f;
+  }
+  info->cells = cells;
+  info->diagonals = diagonals > 0 ? (uint64_t)diagonals : 0;
+  info->tiles = (uint64_t)so.ntiles;
+  info->rows_per_tile = (uint64_t)so.R;
+  info->kernel_launches = launches;
+  info->sweep_ms = so.ms;
+}
+
 int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_config* cfg,
                    uint64_t k_lo64, uint64_t k_hi64, double* d_cmp, int64_t* d_idx,
                    mprof_run_info* info) {
@@ -628,127 +828,23 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   st = carve(c, L, &w);
   if (st != MPROF_OK) return st;
   uint32_t launches = 0;
-  const int g = grid_for(L);
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  st = prepare_operands(c, d_t, n, cfg, w, &launches);
+  if (st != MPROF_OK) return st;
+  k_init_best<<<grid_for(L), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, L);
+  ++launches;
+  SweepOut so;
+  st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, 0, &launches, &so);
+  if (st != MPROF_OK) return st;
   if (zn) {
-    c->stats_t = nullptr;  // force: the series bytes behind d_t may have changed
-    st = ensure_znorm_stats(c, d_t, n64, cfg, w);
+    st = flat_fix(c, w.B, L, (int)k_lo, (int)k_hi, w, w.best, &launches);
     if (st != MPROF_OK) return st;
-    k_init_best<<<g, 256, 0, c->stream>>>(w.best, w.B, L);
-    k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
-    launches += 3;
-    // filter form for this series: MPROF_ZN_FILTER=cov|col overrides the measured choice
-    const char* force = getenv("MPROF_ZN_FILTER");
-    if (force && !strcmp(force, "cov")) {
-      c->zn_colscale = false;
-    } else if (force && !strcmp(force, "col")) {
-      c->zn_colscale = true;
-    } else {
-      if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
-      CK(cudaMemsetAsync(c->d_spread, 0, 2 * sizeof(double), c->stream));
-      k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.B, L, c->d_spread);
-      double h[2];
-      CK(cudaMemcpyAsync(h, c->d_spread, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      ++launches;
-      c->zn_colscale = !(h[1] > 0.0 && h[0] / h[1] >= kZnCovFilterMinSpread);
-    }
-  } else {
-    k_init_best<<<g, 256, 0, c->stream>>>(w.best, nullptr, L);
-    ++launches;
-    // the fast Euclidean policy slides (delta, sigma) pairs; everything else the raw pairs
-    const bool ds = !cfg->exact && (cfg->family == MPROF_EUCLIDEAN ||
-                                    (cfg->family == MPROF_PNORM && cfg->p == 2.0));
-    k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m, ds ? kPairsDeltaSum : kPairsRaw);
-    ++launches;
   }
-  if (cfg->precision == MPROF_FP32) {
-    if (zn) {
-      k_znorm_pairs32<<<g, 256, 0, c->stream>>>(w.A, w.B, w.A32, w.B32, L);
-      ++launches;
-    } else {
-      CK(cudaMemsetAsync(w.scalars, 0, sizeof(double), c->stream));
-      k_mean<<<grid_for(n), 256, 0, c->stream>>>(d_t, n, w.scalars);
-      const bool ds32 = cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0;
-      k_build_pairs32<<<g, 256, 0, c->stream>>>(d_t, w.A32, L, m, ds32 ? kPairsDeltaSum : kPairsRaw,
-                                                w.scalars);
-      launches += 2;
-    }
-  }
-  CK(cudaGetLastError());
-  float ms = 0.f;
-  long long ntiles = 0, R = 0;
-  unsigned long long cells = 0;
-  if (k_lo < k_hi) {
-    R = choose_R(cfg, L, (int)k_lo, (int)k_hi, c->num_sms);
-    st = build_tiles(c, L, (int)k_lo, (int)k_hi, R, &ntiles);
-    if (st != MPROF_OK) return st;
-    SweepParams prm;
-    prm.t = d_t;
-    prm.A = w.A;
-    prm.B = w.B;
-    prm.A32 = w.A32;
-    prm.B32 = w.B32;
-    prm.mu = w.mu;
-    prm.best = w.best;
-    prm.tiles = c->tiles_d;
-    prm.n = n;
-    prm.m = m;
-    prm.L = L;
-    prm.k_hi = (int)k_hi;
-    prm.R = (int)std::min<long long>(R, INT_MAX);
-    prm.p = cfg->p;
-    prm.stats = nullptr;
-    const bool want_stats = getenv("MPROF_STATS") != nullptr;
-    if (want_stats) {
-      CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
-      CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
-    }
-    st = dispatch_sweep(c, cfg, prm, ntiles, (int)k_lo, &launches, &ms);
-    if (st != MPROF_OK) return st;
-    if (want_stats) {
-      unsigned long long h[2];
-      CK(cudaMemcpyAsync(h, prm.stats, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      cudaFreeAsync(prm.stats, c->stream);
-      fprintf(stderr, "[mprof stats] family %d L %d tiles %lld R %lld: replays %llu offers %llu\n",
-              cfg->family, L, ntiles, R, h[0], h[1]);
-    }
-    if (zn) {
-      const int nch = (L + kChunk - 1) / kChunk;
-      k_flat_chunk_min<<<nch, 256, 0, c->stream>>>(w.B, L, w.cmin);
-      k_flat_fix<<<g, 256, 0, c->stream>>>(w.B, L, (int)k_lo, (int)k_hi, w.cmin, w.best);
-      launches += 2;
-      CK(cudaGetLastError());
-    }
-    cells = mprof_band_cells(n64, cfg->m, (uint64_t)k_lo, (uint64_t)k_hi);
-  }
-  k_split<<<g, 256, 0, c->stream>>>(w.best, d_cmp, d_idx, L);
+  k_split<<<grid_for(L), 256, 0, c->stream>>>(w.best, d_cmp, d_idx, L);
   ++launches;
   CK(cudaGetLastError());
-  if (info) {
-    // FP64-pipe instructions per cell of the hot loop (SASS-audited)
-    float ops = 4.f;
-    if (cfg->family == MPROF_ZNORMALIZED) ops = c->zn_colscale ? 3.125f : 2.f;
-    else if (cfg->exact) ops = (cfg->family == MPROF_PNORM && cfg->p != 1.0 && cfg->p != 2.0) ? 8.f : 6.f;
-    else if (cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0) ops = 3.f;
-    else if (cfg->p == 1.0) ops = 4.f;
-    else if (cfg->p == 3.0 || cfg->p == 4.0) ops = 6.f;
-    else ops = 0.f;  // generic pow: library call, not a fixed count
-    if (cfg->precision == MPROF_FP32) {
-      info->fp64_ops_per_cell = 0.f;
-      info->fp32_ops_per_cell = ops;
-    } else {
-      info->fp64_ops_per_cell = ops;
-      info->fp32_ops_per_cell = 0.f;
-    }
-    info->cells = cells;
-    info->diagonals = k_hi > k_lo ? (uint64_t)(k_hi - k_lo) : 0;
-    info->tiles = (uint64_t)ntiles;
-    info->rows_per_tile = (uint64_t)R;
-    info->kernel_launches = launches;
-    info->sweep_ms = ms;
-  }
+  const uint64_t cells = k_lo < k_hi ? mprof_band_cells(n64, cfg->m, (uint64_t)k_lo, (uint64_t)k_hi) : 0;
+  fill_info(c, cfg, cells, k_hi - k_lo, so, launches, info);
   return MPROF_OK;
 }
 
@@ -999,6 +1095,176 @@ int32_t mprof_band_cuts(uint64_t n, uint64_t m, uint64_t exclusion, uint32_t par
     lo = a;
   }
   return MPROF_OK;
+}
+
+// ---- EngineState ---------------------------------------------------------------------------
+
+int32_t mprof_state_build(mprof_ctx* in, const double* t, uint64_t n, const mprof_config* cfg,
+                          mprof_state** out, mprof_run_info* info) {
+  if (!t || !cfg || !out) return fail(MPROF_E_BAD_ARG, "null argument");
+  *out = nullptr;
+  int32_t st = check_series(t, n);
+  if (st != MPROF_OK) return st;
+  st = check_config(n, cfg);
+  if (st != MPROF_OK) return st;
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  mprof_state* S = new mprof_state();
+  S->ctx = c;
+  S->cfg = *cfg;
+  S->n = n;
+  const uint64_t L = n - cfg->m + 1;
+  st = ensure(reinterpret_cast<void**>(&S->t), &S->t_bytes, n * sizeof(double));
+  if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&S->cmp), &S->cmp_bytes, L * sizeof(double));
+  if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&S->idx), &S->idx_bytes, L * sizeof(int64_t));
+  if (st != MPROF_OK) { mprof_state_destroy(S); return st; }
+  cudaError_t e = cudaMemcpyAsync(S->t, t, n * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) { mprof_state_destroy(S); return cuda_fail(e, "cudaMemcpyAsync"); }
+  st = sweep_impl(c, S->t, n, cfg, 0, 0, S->cmp, S->idx, info);
+  if (st != MPROF_OK) { mprof_state_destroy(S); return st; }
+  *out = S;
+  return MPROF_OK;
+}
+
+int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count,
+                           mprof_run_info* info) {
+  if (!S) return fail(MPROF_E_BAD_ARG, "null state");
+  if (count == 0) {
+    if (info) std::memset(info, 0, sizeof *info);
+    return MPROF_OK;  // extend_profile with an empty span returns the state unchanged
+  }
+  if (!samples) return fail(MPROF_E_BAD_ARG, "null samples");
+  for (uint64_t i = 0; i < count; ++i)
+    if (!std::isfinite(samples[i]))
+      return fail(MPROF_E_NON_FINITE, "appended sample %llu is not finite", (unsigned long long)i);
+  mprof_ctx* c = S->ctx;
+  CK(cudaSetDevice(c->device));
+  const mprof_config* cfg = &S->cfg;
+  const uint64_t n_old = S->n, n_new = n_old + count;
+  int32_t st = check_config(n_new, cfg);
+  if (st != MPROF_OK) return st;
+  const int m = (int)cfg->m;
+  const int L_old = (int)(n_old - m + 1), L_new = (int)(n_new - m + 1);
+  const int dL = L_new - L_old;
+  // series: grow (device copy of the old samples), append the new ones
+  if (S->t_bytes < n_new * sizeof(double)) {
+    double* nt = nullptr;
+    size_t cap = 0;
+    st = ensure(reinterpret_cast<void**>(&nt), &cap, std::max<size_t>(n_new * sizeof(double), 2 * S->t_bytes));
+    if (st != MPROF_OK) return st;
+    CK(cudaMemcpyAsync(nt, S->t, n_old * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(S->t);
+    S->t = nt;
+    S->t_bytes = cap;
+  }
+  CK(cudaMemcpyAsync(S->t + n_old, samples, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  st = ensure(reinterpret_cast<void**>(&S->rev), &S->rev_bytes, n_new * sizeof(double));
+  if (st == MPROF_OK) st = ensure(&S->fwd, &S->fwd_bytes, (size_t)L_new * sizeof(BestEntry));
+  if (st != MPROF_OK) return st;
+  uint32_t launches = 0;
+  k_reverse<<<grid_for((long long)n_new), 256, 0, c->stream>>>(S->t, S->rev, (int)n_new);
+  ++launches;
+  // sweep the new cells: rows [0, dL) of every diagonal of the reversed series
+  Workspace w;
+  st = carve(c, L_new, &w);
+  if (st != MPROF_OK) return st;
+  const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  st = prepare_operands(c, S->rev, (int)n_new, cfg, w, &launches);
+  if (st != MPROF_OK) return st;
+  k_init_from_prev<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, S->cmp, S->idx,
+                                                            L_old, L_new);
+  ++launches;
+  SweepOut so;
+  const int k_lo = (int)cfg->exclusion;
+  st = sweep_tiles(c, S->rev, (int)n_new, cfg, w, k_lo, L_new, dL, L_new, &launches, &so);
+  if (st != MPROF_OK) return st;
+  BestEntry* fwd = static_cast<BestEntry*>(S->fwd);
+  k_unreverse<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, fwd, L_new);
+  ++launches;
+  if (zn) {
+    st = ensure_znorm_stats(c, S->t, n_new, cfg, w);  // forward statistics (stats key differs)
+    if (st != MPROF_OK) return st;
+    st = flat_fix(c, w.B, L_new, k_lo, L_new, w, fwd, &launches);
+    if (st != MPROF_OK) return st;
+    ++launches;
+  }
+  st = ensure(reinterpret_cast<void**>(&S->cmp), &S->cmp_bytes, (size_t)L_new * sizeof(double));
+  if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&S->idx), &S->idx_bytes, (size_t)L_new * sizeof(int64_t));
+  if (st != MPROF_OK) return st;
+  k_split<<<grid_for(L_new), 256, 0, c->stream>>>(fwd, S->cmp, S->idx, L_new);
+  ++launches;
+  CK(cudaGetLastError());
+  S->n = n_new;
+  // cells swept: diagonals k in [excl, L_new) contribute min(dL, L_new - k)
+  uint64_t cells = 0;
+  for (long long k = k_lo; k < L_new; ++k) cells += (uint64_t)std::min<long long>(dL, L_new - k);
+  fill_info(c, cfg, cells, L_new - k_lo, so, launches, info);
+  return MPROF_OK;
+}
+
+int32_t mprof_state_clone(const mprof_state* S, mprof_state** out) {
+  if (!S || !out) return fail(MPROF_E_BAD_ARG, "null argument");
+  mprof_ctx* c = S->ctx;
+  CK(cudaSetDevice(c->device));
+  mprof_state* R = new mprof_state();
+  R->ctx = c;
+  R->cfg = S->cfg;
+  R->n = S->n;
+  const uint64_t L = S->n - S->cfg.m + 1;
+  int32_t st = ensure(reinterpret_cast<void**>(&R->t), &R->t_bytes, S->n * sizeof(double));
+  if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&R->cmp), &R->cmp_bytes, L * sizeof(double));
+  if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&R->idx), &R->idx_bytes, L * sizeof(int64_t));
+  if (st != MPROF_OK) { mprof_state_destroy(R); return st; }
+  cudaMemcpyAsync(R->t, S->t, S->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(R->cmp, S->cmp, L * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(R->idx, S->idx, L * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) { mprof_state_destroy(R); return cuda_fail(e, "clone"); }
+  *out = R;
+  return MPROF_OK;
+}
+
+uint64_t mprof_state_series_length(const mprof_state* S) { return S ? S->n : 0; }
+
+int32_t mprof_state_profile(mprof_state* S, double* P, int64_t* I, double* cmp) {
+  if (!S) return fail(MPROF_E_BAD_ARG, "null state");
+  mprof_ctx* c = S->ctx;
+  CK(cudaSetDevice(c->device));
+  const uint64_t L = S->n - S->cfg.m + 1;
+  if (P) {
+    int32_t st = ensure(reinterpret_cast<void**>(&S->P), &S->P_bytes, L * sizeof(double));
+    if (st != MPROF_OK) return st;
+    st = mprof_finalize_device(c, S->t, S->n, S->cmp, S->idx, &S->cfg, S->P);
+    if (st != MPROF_OK) return st;
+    CK(cudaMemcpyAsync(P, S->P, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (I) CK(cudaMemcpyAsync(I, S->idx, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  if (cmp) CK(cudaMemcpyAsync(cmp, S->cmp, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return MPROF_OK;
+}
+
+int32_t mprof_state_series(const mprof_state* S, double* t) {
+  if (!S || !t) return fail(MPROF_E_BAD_ARG, "null argument");
+  CK(cudaSetDevice(S->ctx->device));
+  CK(cudaMemcpyAsync(t, S->t, S->n * sizeof(double), cudaMemcpyDeviceToHost, S->ctx->stream));
+  CK(cudaStreamSynchronize(S->ctx->stream));
+  return MPROF_OK;
+}
+
+void mprof_state_destroy(mprof_state* S) {
+  if (!S) return;
+  if (S->ctx) cudaSetDevice(S->ctx->device);
+  if (S->ctx && S->ctx->stream) cudaStreamSynchronize(S->ctx->stream);
+  cudaFree(S->t);
+  cudaFree(S->cmp);
+  cudaFree(S->idx);
+  cudaFree(S->rev);
+  cudaFree(S->fwd);
+  cudaFree(S->P);
+  delete S;
 }
 
 int32_t mprof_fp64_peak(mprof_ctx* in, double* gflops, float* ms_out) {

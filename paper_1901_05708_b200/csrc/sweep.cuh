@@ -356,9 +356,15 @@ struct SweepParams {
   int n, m, L;
   int k_hi;               // exclusive upper bound of the swept diagonal band
   int R;                  // rows per tile
+  int row_hi;             // exclusive upper bound of the swept rows (L for a full sweep)
+  int rl;                 // index reflection: > 0 stores neighbour indices as rl - 1 - idx
+                          // (sweeps of the time-reversed series, used by the extension)
   double p;
   unsigned long long* stats;  // optional diagnostics (MPROF_STATS): [0] replays [1] offers
 };
+
+// Neighbour index as stored in the profile (original coordinates).
+__device__ __forceinline__ int out_index(int idx, int rl) { return rl > 0 ? rl - 1 - idx : idx; }
 
 template <class P>
 __device__ __forceinline__ const typename P::V2* pairs_of(const SweepParams& prm) {
@@ -406,18 +412,21 @@ struct Acc {
 };
 
 // Exact merge of one flagged cell (rarely reached): column entry first, then the row candidate.
+// Positions (row, j) index the profile being swept; the stored neighbour indices are mapped by
+// out_index (identity except for reflected sweeps) so ties compare in original coordinates.
 __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhit, int row, int j,
-                                        int* ct, BestEntry* best, unsigned long long* rv, int* rj,
-                                        unsigned long long* stats) {
+                                        int rl, int* ct, BestEntry* best, unsigned long long* rv,
+                                        int* rj, unsigned long long* stats) {
   // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
   const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
   if (colhit) {
-    atomicMin(ct, static_cast<int>(offer(best, j, vb, row) >> 32));
+    atomicMin(ct, static_cast<int>(offer(best, j, vb, out_index(row, rl)) >> 32));
     if (stats) atomicAdd(&stats[1], 1ull);
   }
-  if (rowhit && lex_less(vb, j, *rv, *rj)) {
+  const int jo = out_index(j, rl);
+  if (rowhit && lex_less(vb, jo, *rv, *rj)) {
     *rv = vb;
-    *rj = j;
+    *rj = jo;
   }
 }
 
@@ -429,7 +438,7 @@ __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhi
 // (u, d) uses run entry u + d.
 template <class P, int D, bool GUARD>
 __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0, int kt, int kend,
-                                          int L, double p, const typename P::V2* cA1,
+                                          int L, int rl, double p, const typename P::V2* cA1,
                                           const typename P::V2* cA2, const typename P::VB* cB1,
                                           const typename P::VB* cB2, int* cT1, int* cT2,
                                           const typename P::V2* rowA, const typename P::VB* rowB,
@@ -459,7 +468,7 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
       int* ct = e < D ? &cT1[e] : &cT2[e - D];
       const bool rowhit = h <= tr;
       const bool colhit = h <= *reinterpret_cast<volatile int*>(ct);
-      if (rowhit || colhit) merge_cell(v, h, rowhit, colhit, row, row + kt + d, ct, best, &rv, &rj, stats);
+      if (rowhit || colhit) merge_cell(v, h, rowhit, colhit, row, row + kt + d, rl, ct, best, &rv, &rj, stats);
     }
     if (rj != INT_MAX) {
       atomicMin(&rowT[x], static_cast<int>(offer(best, row, rv, rj) >> 32));
@@ -471,7 +480,7 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
 // Merge of the seed cells (every valid cell, all lanes on the same row): columns per cell, the
 // row through a warp lexicographic reduction and one CAS per warp. Called convergently.
 template <int D>
-__device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, int col0,
+__device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, int col0, int rl,
                                           BestEntry* best) {
   unsigned long long rv = kInfBits;
   int rj = INT_MAX;
@@ -481,10 +490,11 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
     const double v = c.v[d];
     const unsigned long long vb = (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
     const int j = col0 + d;
-    offer(best, j, vb, row);
-    if (lex_less(vb, j, rv, rj)) {
+    offer(best, j, vb, out_index(row, rl));
+    const int jo = out_index(j, rl);
+    if (lex_less(vb, jo, rv, rj)) {
       rv = vb;
-      rj = j;
+      rj = jo;
     }
   }
 #pragma unroll
@@ -509,7 +519,7 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 template <class P, int D, int T, int S, bool GUARD>
 __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int X0,
                                           typename P::V (&acc)[D], int i0, int cnt, int kt,
-                                          int kend, int L, BestEntry* best, double p,
+                                          int kend, int L, int rl, BestEntry* best, double p,
                                           unsigned long long* stats) {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
@@ -588,7 +598,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       const int q1 = G::pad((X0 + s + xb) % G::RING);
       const int q2 = G::pad((X0 + s + xb + D) % G::RING);
       int* colT = sm.colT[b];
-      replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, p, &sm.colA[q1], &sm.colA[q2],
+      replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, rl, p, &sm.colA[q1], &sm.colA[q2],
                                 &sm.colB[P::kHasB ? q1 : 0], &sm.colB[P::kHasB ? q2 : 0],
                                 &colT[G::pad(s + xb)], &colT[G::pad(s + xb + D)], rowA,
                                 sm.rowB[b], sm.rowT[b], best, stats);
@@ -708,7 +718,7 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   const int m = prm.m;
   const int kt = kb + static_cast<int>(threadIdx.x) * D;
   const int kend = min(kb + G::K, prm.k_hi);
-  const int re = min(ra + prm.R, L - kb);  // exclusive row end of the tile
+  const int re = min(min(ra + prm.R, L - kb), prm.row_hi);  // exclusive row end of the tile
 
   // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d) --------------------
   double sacc[D];
@@ -776,7 +786,7 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
       c.v[d] = static_cast<double>(P::score(acc[d], rb, cb));
       valid |= (ok ? 1u : 0u) << d;
     }
-    resolve_seed<D>(c, valid, ra, ra + kt, prm.best);
+    resolve_seed<D>(c, valid, ra, ra + kt, prm.rl, prm.best);
   }
 
   // ---- stage pipeline over the row transitions ra .. re-2 ---------------------------------
@@ -802,9 +812,9 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
     const int i0 = ra + s0;
     const bool full = (cnt == S) && (kb + G::K <= prm.k_hi) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {
-      run_stage<P, D, T, S, false>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
+      run_stage<P, D, T, S, false>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.rl, prm.best, prm.p, prm.stats);
     } else {
-      run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
+      run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.rl, prm.best, prm.p, prm.stats);
     }
     if (st + 1 == nst) break;
     cp_async_wait<0>();
