@@ -572,7 +572,7 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long lo
 // __launch_bounds__ minimum CTAs per SM: the policy's own choice if it has one, else the build's.
 template <class P>
 constexpr int min_blocks() {
-  if constexpr (requires { P::kMinBlocks; }) return P::kMinBlocks;
+  if constexpr (requires { P::kMinWarps; }) return std::max(1, P::kMinWarps * 32 / kT);
   else return MPROF_MIN_BLOCKS;
 }
 

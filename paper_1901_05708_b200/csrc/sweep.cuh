@@ -214,7 +214,7 @@ struct Znorm : KeyF64 {
   static constexpr bool kCenteredSeed = true;
   static constexpr bool kCovFilter = true;
   static constexpr bool kColScale = COLSCALE;
-  static constexpr int kMinBlocks = COLSCALE ? 3 : 4;  // measured: the +cB ring wants registers
+  static constexpr int kMinWarps = COLSCALE ? 12 : 16;  // per SM; measured: the +cB ring wants registers
   static constexpr int kPairs = kPairsZnorm;
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     return fma(r.x, c.y, fma(c.x, r.y, acc));
@@ -537,15 +537,14 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
     }
   }
   const V2* rowA = sm.rowA[b];
-  for (int s = 0; s < cnt; s += D) {
-    // the D operands entering during this block are contiguous in the ring: constant offsets
-    const int qn = G::pad((X0 + s + xb + D) % G::RING);
-    const V2* nA = &sm.colA[qn];
-    const VB* nB = &sm.colB[P::kHasB ? qn : 0];
+  // Block threshold (software-pipelined: block s+D's is computed at the start of block s, so its
+  // shared-load -> convert -> multiply chain overlaps the block's FP64 work).
+  // theta: key bound of the block; num: covariance filters' 1 - tau_max (0 = every cell may pass)
+  auto block_theta = [&](int s, int& theta, double& num) {
     const int cb = s / D + threadIdx.x;
     const int tmax = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
-    int theta = P::tau(tmax);
-    double num = 0.0;  // covariance filters: 1 - tau_max (with margin), 0 = every cell may pass
+    theta = P::tau(tmax);
+    num = 0.0;
     if constexpr (P::kCovFilter) {
       if (tmax >= 0x3FF00000) {
         theta = INT_MAX;  // some threshold >= 1: any cell may qualify
@@ -558,6 +557,18 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
         }
       }
     }
+  };
+  int theta_nx;
+  double num_nx;
+  block_theta(0, theta_nx, num_nx);
+  for (int s = 0; s < cnt; s += D) {
+    // the D operands entering during this block are contiguous in the ring: constant offsets
+    const int qn = G::pad((X0 + s + xb + D) % G::RING);
+    const V2* nA = &sm.colA[qn];
+    const VB* nB = &sm.colB[P::kHasB ? qn : 0];
+    const int theta = theta_nx;
+    const double num = num_nx;
+    if (s + D < cnt) block_theta(s + D, theta_nx, num_nx);
     Acc<P, D> acc0;
 #pragma unroll
     for (int d = 0; d < D; ++d) acc0.a[d] = acc[d];
