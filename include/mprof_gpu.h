@@ -123,6 +123,12 @@ void mprof_ctx_destroy(mprof_ctx* ctx);
 int32_t mprof_ctx_set_stream(mprof_ctx* ctx, void* stream);
 /* Time the sweep kernel with CUDA events on the launching stream (fills sweep_ms). */
 int32_t mprof_ctx_set_timing(mprof_ctx* ctx, int32_t enabled);
+/* Anytime observer (ProgressFn, /root/reference/proj/include/mprof/core.hpp:112): when set, the
+ * sweeps of this context run in ascending chunks of diagonals (max(1, total/256) per chunk) and
+ * fn(diagonals_done, diagonals_total, user) is called after each; returning 0 cancels and the
+ * profile holds the exact minimum over the completed diagonals. NULL disables (one launch). */
+typedef int32_t (*mprof_progress_fn)(uint64_t done, uint64_t total, void* user);
+int32_t mprof_ctx_set_progress(mprof_ctx* ctx, mprof_progress_fn fn, void* user);
 
 /* ---- reference entry points (host buffers) ------------------------------------------------ */
 /* P[L] and I[L], L = n - m + 1, caller-allocated. `threads` (reference: CPU workers) selects
@@ -133,6 +139,12 @@ int32_t mprof_aamp_pnorm(mprof_ctx* ctx, const double* t, uint64_t n, const mpro
                          double* P, int64_t* I, mprof_run_info* info);
 int32_t mprof_acamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
                     int32_t variant, double* P, int64_t* I, mprof_run_info* info);
+
+/* Brute-force profile (mprof::brute_profile, /root/reference/proj/src/oracle.cpp:95-132): direct
+ * distances for every admissible pair with the reference's evaluation order, ties to the smallest
+ * j; any family. O(L^2 m) on the GPU — the CLI's `--engine oracle` and an exact checker. */
+int32_t mprof_brute_profile(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                            double* P, int64_t* I);
 
 /* ---- device-resident pipeline ------------------------------------------------------------- */
 /* Sweeps diagonals k in [k_lo, k_hi) ∩ [exclusion, n - m] of series d_t (device, n doubles) and

@@ -31,7 +31,7 @@ __all__ = [
     "profile_length", "default_flat_threshold", "MatrixProfile", "RunInfo", "aamp",
     "aamp_pnorm", "acamp", "sweep_device", "finalize_device", "merge_device", "band_cuts",
     "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context", "EngineState",
-    "build_engine_state", "extend_profile",
+    "build_engine_state", "extend_profile", "brute_profile",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libmprof_gpu.so"
@@ -254,7 +254,11 @@ EXPORTS = {
     "mprof_state_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mprof_state_series": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "mprof_state_destroy": (None, [C.c_void_p]),
+    "mprof_ctx_set_progress": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mprof_brute_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                        C.c_void_p, C.c_void_p]),
 }
+PROGRESS_FN = C.CFUNCTYPE(C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p)
 
 _lib = None
 
@@ -358,12 +362,30 @@ def _run(fn_name: str, ts: TimeSeries, cfg: ProfileConfig, extra, ctx, progress)
     c = _to_c(cfg)
     args = [_ctx_handle(ctx), v.ctypes.data, n, C.byref(c), *extra, P.ctypes.data, I.ctypes.data,
             C.byref(info)]
-    _raise(getattr(lib(), fn_name)(*args))
+    cb = None
     if progress is not None:
-        # The sweep is one device launch: the observer fires once, at completion
-        # (diagonals_done == diagonals_total). Its return value cannot cancel finished work.
-        progress(int(info.diagonals), int(info.diagonals))
+        # anytime observer (ProgressFn): band-granular chunks, False cancels
+        cb = PROGRESS_FN(lambda done, total, _u: 1 if progress(int(done), int(total)) else 0)
+        _raise(lib().mprof_ctx_set_progress(_ctx_handle(ctx), C.cast(cb, C.c_void_p), None))
+    try:
+        _raise(getattr(lib(), fn_name)(*args))
+    finally:
+        if cb is not None:
+            lib().mprof_ctx_set_progress(_ctx_handle(ctx), None, None)
     return MatrixProfile(P, I, cfg.m, cfg.kind, info)
+
+
+def brute_profile(ts: TimeSeries, cfg: ProfileConfig, ctx: Optional[Context] = None) -> MatrixProfile:
+    """mprof::brute_profile (/root/reference/proj/include/mprof/oracle.hpp:20) on the GPU."""
+    _check_int_fields(cfg)
+    v = ts.values()
+    L = max(v.shape[0] - cfg.m + 1, 0)
+    P = np.empty(L)
+    I = np.empty(L, dtype=np.int64)
+    c = _to_c(cfg)
+    _raise(lib().mprof_brute_profile(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
+                                     P.ctypes.data, I.ctypes.data))
+    return MatrixProfile(P, I, cfg.m, cfg.kind)
 
 
 def aamp(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Callable] = None, threads: int = 0,

@@ -17,6 +17,7 @@ ROOT = Path(__file__).resolve().parent.parent
 PKG = ROOT / "paper_1901_05708_b200"
 CSRC = PKG / "csrc"
 LIB = PKG / "libmprof_gpu.so"
+CLI = PKG / "bin" / "mprof"
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -25,7 +26,7 @@ NVFLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler"
 
 
 def _sources():
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))  # csrc/cli is the executable
 
 
 def _deps():
@@ -68,6 +69,18 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_cli(force: bool = False) -> Path:
+    """The `mprof` command line front end (C++, links libmprof_gpu.so via rpath)."""
+    src = CSRC / "cli" / "mprof_main.cpp"
+    deps = [src, LIB] + sorted((ROOT / "include").rglob("*.h*"))
+    if not force and not _stale(CLI, deps):
+        return CLI
+    CLI.parent.mkdir(parents=True, exist_ok=True)
+    _run(["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), str(src), "-L", str(PKG),
+          "-lmprof_gpu", "-Wl,-rpath,$ORIGIN/..", "-o", str(CLI)])
+    return CLI
+
+
 def build_oracle(force: bool = False) -> None:
     """Builds oracle/liboracle.so (always) and oracle/_ref (when /root/reference exists)."""
     _run(["make", "-C", str(ROOT / "oracle"), "all"])
@@ -75,6 +88,7 @@ def build_oracle(force: bool = False) -> None:
 
 def build(force: bool = False, verbose: bool = False) -> None:
     build_gpu(force=force, verbose=verbose)
+    build_cli(force=force)
     build_oracle(force=force)
 
 

@@ -255,6 +255,95 @@ __global__ void k_flat_fix(const double* __restrict__ B, int L, int k_lo, int k_
   }
 }
 
+// ---- brute-force profile (the reference's oracle, /root/reference/proj/src/oracle.cpp:51-132) --
+// Direct distances with the reference's evaluation order (no contraction), the smallest j
+// winning ties. O(L^2 m): a checker and the CLI's `--engine oracle`, not the hot path.
+__global__ void k_moments(const double* __restrict__ t, int L, int m, double* __restrict__ mean,
+                          double* __restrict__ var) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
+    double sum = 0.0, sumsq = 0.0;  // oracle.cpp:35-47
+    for (int l = 0; l < m; ++l) {
+      const double v = t[p + l];
+      sum = __dadd_rn(sum, v);
+      sumsq = __dadd_rn(sumsq, __dmul_rn(v, v));
+    }
+    const double mu = __ddiv_rn(sum, (double)m);
+    double vv = __dsub_rn(__ddiv_rn(sumsq, (double)m), __dmul_rn(mu, mu));
+    if (vv < 0.0) vv = 0.0;
+    mean[p] = mu;
+    var[p] = vv;
+  }
+}
+
+__device__ __forceinline__ double bf_abs_pow(double x, double p) {  // oracle.cpp:17-24
+  const double a = fabs(x);
+  if (p == 1.0) return a;
+  if (p == 2.0) return __dmul_rn(a, a);
+  if (p == 3.0) return __dmul_rn(__dmul_rn(a, a), a);
+  if (p == 4.0) return __dmul_rn(__dmul_rn(a, a), __dmul_rn(a, a));
+  return pow(a, p);
+}
+
+__device__ double bf_dist(const double* __restrict__ t, int i, int j, int m, int family, double p,
+                          double flat, const double* __restrict__ mean,
+                          const double* __restrict__ var) {
+  double sum = 0.0;
+  if (family == MPROF_EUCLIDEAN) {
+    for (int l = 0; l < m; ++l) {
+      const double d = __dsub_rn(t[i + l], t[j + l]);
+      sum = __dadd_rn(sum, __dmul_rn(d, d));
+    }
+    return sqrt(sum);
+  }
+  if (family == MPROF_PNORM) {
+    for (int l = 0; l < m; ++l) sum = __dadd_rn(sum, bf_abs_pow(__dsub_rn(t[i + l], t[j + l]), p));
+    return pow(sum, 1.0 / p);
+  }
+  const double va = var[i], vb = var[j];
+  const bool fa = va <= flat, fb = vb <= flat;
+  if (fa && fb) return 0.0;
+  if (fa || fb) return sqrt(2.0 * (double)m);
+  const double ma = mean[i], mb = mean[j];
+  const double ia = __ddiv_rn(1.0, sqrt(va)), ib = __ddiv_rn(1.0, sqrt(vb));
+  for (int l = 0; l < m; ++l) {
+    const double d = __dsub_rn(__dmul_rn(__dsub_rn(t[i + l], ma), ia), __dmul_rn(__dsub_rn(t[j + l], mb), ib));
+    sum = __dadd_rn(sum, __dmul_rn(d, d));
+  }
+  return sqrt(sum);
+}
+
+// one CTA per row i; lexicographic (distance, j) minimum over admissible j
+__global__ void k_brute(const double* __restrict__ t, int L, int m, int excl, int family, double p,
+                        double flat, const double* __restrict__ mean,
+                        const double* __restrict__ var, double* __restrict__ P,
+                        int64_t* __restrict__ I) {
+  __shared__ double sv[32];
+  __shared__ int sj[32];
+  for (int i = blockIdx.x; i < L; i += gridDim.x) {
+    double bv = INFINITY;
+    int bj = INT_MAX;
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+      if (abs(i - j) < excl) continue;
+      const double d = bf_dist(t, i, j, m, family, p, flat, mean, var);
+      if (d < bv || (d == bv && j < bj)) { bv = d; bj = j; }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+      if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+    }
+    if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = bv; sj[threadIdx.x >> 5] = bj; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (sv[w] < bv || (sv[w] == bv && sj[w] < bj)) { bv = sv[w]; bj = sj[w]; }
+      P[i] = bj == INT_MAX ? INFINITY : bv;
+      I[i] = bj == INT_MAX ? -1 : bj;
+    }
+    __syncthreads();
+  }
+}
+
 // ---- streaming extension (build_engine_state / extend_profile) -----------------------------
 __global__ void k_reverse(const double* __restrict__ in, double* __restrict__ out, int n) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
@@ -414,6 +503,8 @@ struct mprof_ctx {
   double stats_thr = -1.0;
   bool zn_colscale = false;  // z-norm filter form chosen for the current sweep
   double* d_spread = nullptr;
+  mprof_progress_fn progress = nullptr;  // anytime observer (band granularity)
+  void* progress_user = nullptr;
 };
 
 // Device-resident EngineState: the series, the comparison-space profile and scratch.
@@ -834,12 +925,37 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   k_init_best<<<grid_for(L), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, L);
   ++launches;
   SweepOut so;
-  st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, 0, &launches, &so);
-  if (st != MPROF_OK) return st;
+  long long k_done = k_hi;
+  if (!c->progress || k_lo >= k_hi) {
+    st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, 0, &launches, &so);
+    if (st != MPROF_OK) return st;
+  } else {
+    // Anytime mode (scan_diagonals' observer, /root/reference/proj/src/detail/diag_scan.hpp:
+    // 210-226): the band is swept in ascending chunks of diagonals, the observer sees
+    // (diagonals done, total) after each; false cancels, leaving the exact minimum over the
+    // completed diagonals. Chunks of max(1, total/256) diagonals (one diagonal for small runs).
+    const long long total = k_hi - k_lo;
+    const long long chunk = std::max<long long>(1, (total + 255) / 256);
+    for (long long a = k_lo; a < k_hi; a += chunk) {
+      const long long b = std::min(k_hi, a + chunk);
+      SweepOut part;
+      st = sweep_tiles(c, d_t, n, cfg, w, (int)a, (int)b, L, 0, &launches, &part);
+      if (st != MPROF_OK) return st;
+      so.ms += part.ms;
+      so.ntiles += part.ntiles;
+      so.R = part.R;
+      CK(cudaStreamSynchronize(c->stream));
+      if (!c->progress((uint64_t)(b - k_lo), (uint64_t)total, c->progress_user)) {
+        k_done = b;
+        break;
+      }
+    }
+  }
   if (zn) {
-    st = flat_fix(c, w.B, L, (int)k_lo, (int)k_hi, w, w.best, &launches);
+    st = flat_fix(c, w.B, L, (int)k_lo, (int)k_done, w, w.best, &launches);
     if (st != MPROF_OK) return st;
   }
+  k_hi = k_done;
   k_split<<<grid_for(L), 256, 0, c->stream>>>(w.best, d_cmp, d_idx, L);
   ++launches;
   CK(cudaGetLastError());
@@ -1265,6 +1381,48 @@ void mprof_state_destroy(mprof_state* S) {
   cudaFree(S->fwd);
   cudaFree(S->P);
   delete S;
+}
+
+int32_t mprof_ctx_set_progress(mprof_ctx* in, mprof_progress_fn fn, void* user) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  c->progress = fn;
+  c->progress_user = user;
+  return MPROF_OK;
+}
+
+int32_t mprof_brute_profile(mprof_ctx* in, const double* t, uint64_t n, const mprof_config* cfg,
+                            double* P, int64_t* I) {
+  if (!t || !cfg || !P || !I) return fail(MPROF_E_BAD_ARG, "null argument");
+  int32_t st = check_series(t, n);
+  if (st != MPROF_OK) return st;
+  st = check_config(n, cfg);  // brute_profile validates but accepts every family
+  if (st != MPROF_OK) return st;
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  const uint64_t L = n - cfg->m + 1;
+  const size_t nt = align_up(n * sizeof(double)), nl = align_up(L * sizeof(double));
+  st = ensure(&c->io, &c->io_bytes, nt + 4 * nl);
+  if (st != MPROF_OK) return st;
+  char* base = static_cast<char*>(c->io);
+  double* d_t = reinterpret_cast<double*>(base);
+  double* d_P = reinterpret_cast<double*>(base + nt);
+  int64_t* d_I = reinterpret_cast<int64_t*>(base + nt + nl);
+  double* d_mean = reinterpret_cast<double*>(base + nt + 2 * nl);
+  double* d_var = reinterpret_cast<double*>(base + nt + 3 * nl);
+  CK(cudaMemcpyAsync(d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (cfg->family == MPROF_ZNORMALIZED)
+    k_moments<<<grid_for((long long)L), 256, 0, c->stream>>>(d_t, (int)L, (int)cfg->m, d_mean, d_var);
+  k_brute<<<(unsigned)std::min<uint64_t>(L, 148ull * 64), 256, 0, c->stream>>>(
+      d_t, (int)L, (int)cfg->m, (int)cfg->exclusion, cfg->family, cfg->p, cfg->flat_threshold,
+      d_mean, d_var, d_P, d_I);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(P, d_P, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(I, d_I, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return MPROF_OK;
 }
 
 int32_t mprof_fp64_peak(mprof_ctx* in, double* gflops, float* ms_out) {

@@ -1,12 +1,15 @@
 // mprof_shim.cpp — the C++ drop-in API (include/mprof/*.hpp) over the C ABI.
-// Replaces the reference's src/aamp.cpp, src/acamp.cpp and src/core.cpp for a GPU build:
-// same validation order and error codes, MatrixProfile returned by value.
+// Replaces the reference's src/aamp.cpp, src/acamp.cpp, src/core.cpp, src/oracle.cpp
+// (brute_profile) and src/engine_state.cpp for a GPU build: same validation order and error
+// codes, MatrixProfile returned by value.
 #include <cmath>
 #include <string>
 
 #include "mprof/aamp.hpp"
 #include "mprof/acamp.hpp"
 #include "mprof/core.hpp"
+#include "mprof/engine_state.hpp"
+#include "mprof/oracle.hpp"
 #include "mprof_gpu.h"
 
 namespace mprof {
@@ -32,6 +35,22 @@ mprof_config to_c(const ProfileConfig& cfg) {
   return c;
 }
 
+// The observer runs on the calling thread between band launches; false cancels.
+int32_t progress_trampoline(uint64_t done, uint64_t total, void* user) {
+  const ProgressFn& fn = *static_cast<const ProgressFn*>(user);
+  return fn(static_cast<std::size_t>(done), static_cast<std::size_t>(total)) ? 1 : 0;
+}
+
+struct ProgressScope {
+  explicit ProgressScope(const ProgressFn& fn) : active(static_cast<bool>(fn)) {
+    if (active) mprof_ctx_set_progress(nullptr, progress_trampoline, const_cast<ProgressFn*>(&fn));
+  }
+  ~ProgressScope() {
+    if (active) mprof_ctx_set_progress(nullptr, nullptr, nullptr);
+  }
+  bool active;
+};
+
 template <class Call>
 MatrixProfile run(const TimeSeries& ts, const ProfileConfig& cfg, const ProgressFn& progress,
                   Call&& call) {
@@ -44,9 +63,12 @@ MatrixProfile run(const TimeSeries& ts, const ProfileConfig& cfg, const Progress
   out.distances.resize(len);
   out.nn_index.resize(len);
   mprof_run_info info{};
-  const int32_t st = call(&c, out.distances.data(), out.nn_index.data(), &info);
+  int32_t st;
+  {
+    ProgressScope scope(progress);
+    st = call(&c, out.distances.data(), out.nn_index.data(), &info);
+  }
   if (st != MPROF_OK) rethrow(st);
-  if (progress) progress(info.diagonals, info.diagonals);
   return out;
 }
 
@@ -88,6 +110,60 @@ MatrixProfile acamp(const TimeSeries& ts, const ProfileConfig& cfg, AcampVariant
   return run(ts, cfg, progress, [&](const mprof_config* c, double* P, int64_t* I, mprof_run_info* info) {
     return mprof_acamp(nullptr, ts.data(), ts.size(), c, v, P, I, info);
   });
+}
+
+MatrixProfile brute_profile(const TimeSeries& ts, const ProfileConfig& cfg) {
+  return run(ts, cfg, {}, [&](const mprof_config* c, double* P, int64_t* I, mprof_run_info*) {
+    return mprof_brute_profile(nullptr, ts.data(), ts.size(), c, P, I);
+  });
+}
+
+// ---- EngineState -----------------------------------------------------------------------------
+
+namespace {
+
+EngineState snapshot(std::shared_ptr<mprof_state> dev, const ProfileConfig& cfg) {
+  const uint64_t n = mprof_state_series_length(dev.get());
+  const uint64_t L = n - cfg.m + 1;
+  std::vector<double> t(n), P(L), cmp(L);
+  std::vector<Index> I(L);
+  int32_t st = mprof_state_series(dev.get(), t.data());
+  if (st == MPROF_OK) st = mprof_state_profile(dev.get(), P.data(), I.data(), cmp.data());
+  if (st != MPROF_OK) rethrow(st);
+  MatrixProfile mp;
+  mp.distances = std::move(P);
+  mp.nn_index = std::move(I);
+  mp.m = cfg.m;
+  mp.kind = cfg.kind;
+  return EngineState{make_time_series(std::move(t)), cfg, std::move(mp), std::move(cmp), std::move(dev)};
+}
+
+}  // namespace
+
+EngineState build_engine_state(const TimeSeries& ts, const ProfileConfig& cfg, ProgressFn progress,
+                               unsigned) {
+  const mprof_config c = to_c(cfg);
+  mprof_state* raw = nullptr;
+  int32_t st;
+  {
+    ProgressScope scope(progress);
+    st = mprof_state_build(nullptr, ts.data(), ts.size(), &c, &raw, nullptr);
+  }
+  if (st != MPROF_OK) rethrow(st);
+  return snapshot(std::shared_ptr<mprof_state>(raw, mprof_state_destroy), cfg);
+}
+
+EngineState extend_profile(const EngineState& state, std::span<const double> new_samples) {
+  for (std::size_t i = 0; i < new_samples.size(); ++i)
+    if (!std::isfinite(new_samples[i]))
+      throw Error(ErrorCode::NonFinite, "appended sample " + std::to_string(i) + " is not finite");
+  mprof_state* raw = nullptr;
+  int32_t st = mprof_state_clone(state.device.get(), &raw);
+  if (st != MPROF_OK) rethrow(st);
+  std::shared_ptr<mprof_state> dev(raw, mprof_state_destroy);
+  st = mprof_state_extend(dev.get(), new_samples.data(), new_samples.size(), nullptr);
+  if (st != MPROF_OK) rethrow(st);
+  return snapshot(std::move(dev), state.cfg);
 }
 
 }  // namespace mprof
