@@ -210,7 +210,8 @@ def main():
     import torch.distributed as dist
     import paper_1901_05708_b200 as mp
     from paper_1901_05708_b200 import workloads as W
-    from paper_1901_05708_b200.distributed import band_for_rank, merge_min_
+    from paper_1901_05708_b200.distributed import (band_for_rank, finalize_sharded, merge_min_,
+                                                   shard_size)
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -230,9 +231,10 @@ def main():
     band = band_for_rank(n, m, 1, rank, world)
     with torch.cuda.stream(stream):
         d_t = torch.tensor(t, dtype=torch.float64, device="cuda")
+        Lp = world * shard_size(L, world)  # P padded to equal all-gather slices
         bufs = {e: (torch.empty(L, dtype=torch.float64, device="cuda"),
                     torch.empty(L, dtype=torch.int64, device="cuda"),
-                    torch.empty(L, dtype=torch.float64, device="cuda")) for e in engines}
+                    torch.empty(Lp, dtype=torch.float64, device="cuda")) for e in engines}
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
     stream.synchronize()
 
@@ -249,8 +251,10 @@ def main():
                                        idx.data_ptr(), ctx=ctx)
                 if world > 1:
                     merge_min_(cmp, idx)
-                mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
-                                   P.data_ptr(), ctx=ctx)
+                    finalize_sharded(mp, d_t.data_ptr(), n, cmp, idx, cfgs[e], P, ctx=ctx)
+                else:
+                    mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
+                                       P.data_ptr(), ctx=ctx)
                 if record:
                     sweep_ms[e].append(info.sweep_ms)
                     ops_per_cell[e] = info.fp64_ops_per_cell
@@ -326,7 +330,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": {"workload": f"C4 {'+'.join(engines)}: n={n}, m={m}, exclusion 1, FP64, "
-                                   f"{'equal-area diagonal bands + ncclMin merge' if world > 1 else 'single GPU'}",
+                                   f"{'equal-area diagonal bands + ncclMin merge + sharded finalize' if world > 1 else 'single GPU'}",
                        "n": n, "m": m, "engines": engines, "cells_per_step": total_cells,
                        "l2": "flushed every step (256 MiB memset inside the timed region)",
                        "parallelism": f"diagonal-band dp{world}"},
@@ -346,6 +350,7 @@ def main():
 
 def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, stream):
     import ctypes as C
+    from paper_1901_05708_b200 import distributed as D
     L = n - m + 1
     h_t = torch.from_numpy(t).pin_memory()
     h_P = torch.empty(L, dtype=torch.float64).pin_memory()
@@ -369,16 +374,14 @@ def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, s
                 for e in engines:
                     cmp = torch.empty(L, dtype=torch.float64, device="cuda")
                     idx = torch.empty(L, dtype=torch.int64, device="cuda")
-                    P = torch.empty(L, dtype=torch.float64, device="cuda")
+                    P = torch.empty(world * D.shard_size(L, world), dtype=torch.float64,
+                                    device="cuda")
                     stream.synchronize()
                     mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], cmp.data_ptr(),
                                     idx.data_ptr(), ctx=ctx)
-                    merge_min = __import__("paper_1901_05708_b200.distributed",
-                                           fromlist=["merge_min_"]).merge_min_
-                    merge_min(cmp, idx)
-                    mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
-                                       P.data_ptr(), ctx=ctx)
-                    h_P.copy_(P, non_blocking=True)
+                    D.merge_min_(cmp, idx)
+                    D.finalize_sharded(mp, d_t.data_ptr(), n, cmp, idx, cfgs[e], P, ctx=ctx)
+                    h_P.copy_(P[:L], non_blocking=True)
                     h_I.copy_(idx, non_blocking=True)
                 stream.synchronize()
 
@@ -399,7 +402,7 @@ def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, s
     return {"value": total / el, "unit": UNIT, "h2d_bytes_per_step": 8 * n * len(engines),
             "d2h_bytes_per_step": 16 * L * len(engines),
             "path": "C ABI host entry points mprof_aamp / mprof_acamp (pinned host buffers)"
-                    if world == 1 else "mprof_sweep_device + ncclMin merge + mprof_finalize_device, H2D/D2H pinned",
+                    if world == 1 else "mprof_sweep_device + ncclMin merge + sharded mprof_finalize_range_device + all-gather, H2D/D2H pinned",
             "ms_per_step": el / args.steps * 1e3}
 
 

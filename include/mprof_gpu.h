@@ -164,6 +164,12 @@ int32_t mprof_sweep_device(mprof_ctx* ctx, const double* d_t, uint64_t n, const 
  * conversion of the comparison value. Untouched entries (idx -1) stay +inf. */
 int32_t mprof_finalize_device(mprof_ctx* ctx, const double* d_t, uint64_t n, const double* d_cmp,
                               const int64_t* d_idx, const mprof_config* cfg, double* d_P);
+/* Entries [lo, hi) only (d_P indexed absolutely): ranks of a multi-GPU run finalize disjoint
+ * slices of the merged profile and all-gather them. */
+int32_t mprof_finalize_range_device(mprof_ctx* ctx, const double* d_t, uint64_t n,
+                                    const double* d_cmp, const int64_t* d_idx,
+                                    const mprof_config* cfg, double* d_P, uint64_t lo,
+                                    uint64_t hi);
 /* Lexicographic (cmp, idx) merge of two partial profiles in place into (d_cmp, d_idx):
  * the fused peer-memory alternative to the two-pass ncclMin merge. d_other_* may be peer
  * pointers (NVLink) when peer access is enabled. */
@@ -193,7 +199,9 @@ void mprof_state_destroy(mprof_state* st);
 
 /* ---- multi-GPU partition (host-side math, no device needed) ------------------------------ */
 /* Equal-area cut of the diagonal range [exclusion, n-m] into `parts` contiguous bands; writes
- * parts+1 boundaries (cuts[0] = exclusion, cuts[parts] = n-m+1). Area(k) = L - k cells. */
+ * parts+1 boundaries (cuts[0] = exclusion, cuts[parts] = n-m+1). Area(k) = L - k cells. Interior
+ * cuts are rounded to the nearest exclusion + 1 + multiple of 1024 (whole tile-grid diagonal
+ * blocks), which moves at most 512 diagonals. */
 int32_t mprof_band_cuts(uint64_t n, uint64_t m, uint64_t exclusion, uint32_t parts,
                         uint64_t* cuts);
 /* Cells of band [k_lo, k_hi): sum_{k} (L - k). */

@@ -242,6 +242,9 @@ EXPORTS = {
                                           C.c_void_p, C.POINTER(_Config), C.c_void_p]),
     "mprof_merge_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_uint64]),
+    "mprof_finalize_range_device": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                                C.c_void_p, C.POINTER(_Config), C.c_void_p,
+                                                C.c_uint64, C.c_uint64]),
     "mprof_band_cuts": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
                                     C.POINTER(C.c_uint64)]),
     "mprof_band_cells": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),
@@ -424,6 +427,13 @@ def finalize_device(d_t: int, n: int, d_cmp: int, d_idx: int, cfg: ProfileConfig
     c = _to_c(cfg)
     _raise(lib().mprof_finalize_device(_ctx_handle(ctx), C.c_void_p(d_t), n, C.c_void_p(d_cmp),
                                        C.c_void_p(d_idx), C.byref(c), C.c_void_p(d_P)))
+
+
+def finalize_range_device(d_t: int, n: int, d_cmp: int, d_idx: int, cfg: ProfileConfig, d_P: int,
+                          lo: int, hi: int, ctx: Optional[Context] = None) -> None:
+    c = _to_c(cfg)
+    _raise(lib().mprof_finalize_range_device(_ctx_handle(ctx), C.c_void_p(d_t), n, C.c_void_p(d_cmp),
+                                             C.c_void_p(d_idx), C.byref(c), C.c_void_p(d_P), lo, hi))
 
 
 def merge_device(d_cmp: int, d_idx: int, d_ocmp: int, d_oidx: int, L: int,

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -173,9 +174,9 @@ __global__ void k_bspread(const double* __restrict__ B, int L, double* out) {
   }
 }
 
-// Thresholds from the band's first diagonal k1: every cell (i, i+k1) evaluated directly and
-// merged exactly. These are genuine cells of the band, so the result is unchanged; they only
-// give the high-word filter near-final thresholds before the tiles start.
+// Thresholds from diagonal k1 = exclusion: every cell (i, i+k1) evaluated directly and merged
+// exactly. These are genuine cells, so the (merged) result is unchanged; they only give the
+// high-word filter near-final thresholds before the tiles start.
 template <class PP>
 __global__ void k_first_diag(SweepParams prm, int k1) {
   using P = typename PP::Base;  // FP64 evaluation, also in FP32 mode
@@ -394,13 +395,13 @@ __global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__
 // and near-duplicate z-normalized windows come out at ~1e-14 instead of sqrt(eps). Flat rules
 // as f_value / dist_znorm (acamp.hpp:52-57, oracle.cpp:81-84). In the exact (parity) mode the
 // reference's own conversion of the comparison value is applied.
-__global__ void k_finalize(const double* __restrict__ t, const double* __restrict__ cmp,
-                           const int64_t* __restrict__ idx, const double* __restrict__ mu,
-                           const double* __restrict__ B, double* __restrict__ P, int L, int m,
-                           int family, double p, int exact) {
+__global__ void k_finalize_range(const double* __restrict__ t, const double* __restrict__ cmp,
+                                 const int64_t* __restrict__ idx, const double* __restrict__ mu,
+                                 const double* __restrict__ B, double* __restrict__ P, int lo, int hi,
+                                 int m, int family, double p, int exact) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < L; i += warps) {
+  for (int i = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < hi; i += warps) {
     const double v = cmp[i];
     const long long j = idx[i];
     const double md = (double)m;
@@ -485,6 +486,8 @@ struct mprof_ctx {
   bool own_stream = false;
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t side = nullptr;  // concurrent near-diagonal z-norm tiles
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sms = 148;
   // grow-only device workspace
   void* ws = nullptr;
@@ -493,8 +496,8 @@ struct mprof_ctx {
   void* io = nullptr;
   size_t io_bytes = 0;
   // tile table cache
-  std::vector<int2> tiles_h;
-  int2* tiles_d = nullptr;
+  std::vector<int4> tiles_h;  // (first diagonal, first row, row end, -)
+  int4* tiles_d = nullptr;
   size_t tiles_cap = 0;
   long long tiles_key[6] = {-1, -1, -1, -1, -1, -1};
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
@@ -615,43 +618,115 @@ int32_t ensure_znorm_stats(mprof_ctx* c, const double* d_t, uint64_t n, const mp
 // diag_scan.hpp:97-104) or runs whole diagonals; the fast mode balances seeding cost (m/(2R) of
 // the cell work) against having enough tiles for every SM.
 // Rows of diagonal block kb that hold cells: [0, min(L - kb, row_hi)).
-long long count_tiles(int L, int k_lo, int k_hi, int row_hi, long long R) {
+// Rows per tile of a diagonal block w < K diagonals wide (a band's last block): a narrow tile is
+// latency-bound per row (a thin tile of R rows costs ~3/4 of a full one), so its rows shrink with
+// its width. Exact mode keeps R: runs are seeded at multiples of refresh_interval.
+long long block_R(long long R, long long w, bool exact) {
+  if (exact || w >= kK) return R;
+  return std::min(R, std::max<long long>(2 * kS, (R * w / kK + kS - 1) / kS * kS));
+}
+
+long long count_tiles(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact = false) {
   long long t = 0;
-  for (long long kb = k_lo; kb < k_hi; kb += kK)
-    t += (std::min<long long>(L - kb, row_hi) + R - 1) / R;
+  for (long long kb = k_lo; kb < k_hi; kb += kK) {
+    const long long Rb = block_R(R, std::min<long long>(kK, k_hi - kb), exact);
+    t += (std::min<long long>(L - kb, row_hi) + Rb - 1) / Rb;
+  }
   return t;
 }
 
-long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int num_sms) {
+// Cells of tile (kb, ra) (diagonals [kb, min(kb + K, k_hi)), rows [ra, min(ra + R, row_hi)),
+// diagonal k ends at row L - k): sum over k of clamp(min(A, B - k), 0), A = rows cap, B = L - ra.
+double tile_cells(long long L, long long kb, long long k_hi, long long row_hi, long long ra, long long R) {
+  const long long k0 = kb, k1 = std::min<long long>(kb + kK, k_hi);
+  const long long A = std::min(R, row_hi - ra), B = L - ra;
+  if (A <= 0 || k0 >= k1) return 0.0;
+  const long long kf = std::clamp(B - A, k0, k1);  // k < kf: full A rows
+  const long long ke = std::clamp(B, k0, k1);      // kf <= k < ke: B - k rows
+  const double full = (double)(kf - k0) * (double)A;
+  const double tri = (double)(ke - kf) * (double)B - 0.5 * (double)(ke - 1 + kf) * (double)(ke - kf);
+  return full + tri;
+}
+
+// Makespan (in row-steps of a full-width tile) of the tile list in launch order on `slots`
+// resident CTAs: the block scheduler hands the next tile to the first free slot (list
+// scheduling). Per-tile fixed cost: the FP64 seeds (m per diagonal, ~1/3 of a row-step each in
+// FP64-pipe terms) plus pipeline fill.
+double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int slots, int m) {
+  std::vector<double> heap(slots, 0.0);  // min-heap of slot free times
+  auto cmp = std::greater<double>();
+  const double fixed = (double)m / 3.0 + 2.0 * kS;
+  double makespan = 0.0;
+  for (long long kb = k_lo; kb < k_hi; kb += kK) {
+    const long long w = std::min<long long>(kK, k_hi - kb);
+    const long long Rb = block_R(R, w, false);
+    for (long long ra = 0; ra < std::min<long long>(L - kb, row_hi); ra += Rb) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      // narrow tiles: per-row latency floor of a quarter of a full row-step
+      const double cells = tile_cells(L, kb, k_hi, row_hi, ra, Rb);
+      const double end = heap.back() + std::max(cells / kK, cells / w * 0.25) + fixed;
+      heap.back() = end;
+      std::push_heap(heap.begin(), heap.end(), cmp);
+      makespan = std::max(makespan, end);
+    }
+  }
+  return makespan;
+}
+
+// Rows per tile. Longest runs amortise the seeds best (R_max = 32 m rows), but a grid of a few
+// waves loses up to a whole wave to its tail: the candidates R_max / j (stage multiples) are
+// scheduled on the sweep kernel's real residency (slots = occupancy x SMs) and the shortest
+// makespan wins (ties -> longer tiles). Grids beyond 48 waves keep R_max.
+long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int slots) {
   if (cfg->exact) {
     if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
     return L;  // the whole diagonal is one run, like the reference's refresh = 0
   }
-  long long R = std::max<long long>(32LL * (long long)cfg->m, 8LL * kS);
-  R = (R + kS - 1) / kS * kS;
-  const long long want = 16LL * num_sms;
-  while (R > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, R) < want)
-    R = std::max<long long>(2 * kS, (R / 2 + kS - 1) / kS * kS);
-  if (const char* e = getenv("MPROF_ROWS_PER_TILE")) R = std::max(1LL, atoll(e));  // experiments
-  if (cfg->refresh_interval > 0) R = std::min<long long>(R, (long long)cfg->refresh_interval);
+  long long Rmax = std::max<long long>(32LL * (long long)cfg->m, 8LL * kS);
+  Rmax = (Rmax + kS - 1) / kS * kS;
+  if (cfg->refresh_interval > 0) Rmax = std::min<long long>(Rmax, (long long)cfg->refresh_interval);
+  long long R = Rmax;
+  if (const char* e = getenv("MPROF_ROWS_PER_TILE")) return std::max(1LL, atoll(e));  // experiments
+  if (Rmax > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, Rmax) < 48LL * slots) {
+    double best = schedule_makespan(L, k_lo, k_hi, row_hi, Rmax, slots, (int)cfg->m);
+    long long prev = Rmax;
+    for (int j = 2; j <= 64; ++j) {
+      const long long Rj = std::max<long long>(2 * kS, (Rmax / j + kS - 1) / kS * kS);
+      if (Rj >= prev) continue;
+      prev = Rj;
+      if (count_tiles(L, k_lo, k_hi, row_hi, Rj) > 256LL * slots) break;
+      const double ms = schedule_makespan(L, k_lo, k_hi, row_hi, Rj, slots, (int)cfg->m);
+      if (getenv("MPROF_TILE_DEBUG"))
+        fprintf(stderr, "[mprof tiles] slots %d R %lld tiles %lld makespan %.0f (R_max %.0f)\n", slots,
+                Rj, count_tiles(L, k_lo, k_hi, row_hi, Rj), ms, best);
+      if (ms < best * (1.0 - 1e-3)) {
+        best = ms;
+        R = Rj;
+      }
+      if (Rj == 2 * kS) break;
+    }
+  }
   return R;
 }
 
-int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long long R,
+int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long long R, bool exact,
                     long long* ntiles) {
-  const long long key[6] = {L, k_lo, k_hi, R, kK, row_hi};
+  const long long key[6] = {L, k_lo, k_hi, R, exact ? -kK : kK, row_hi};
   if (std::equal(key, key + 6, c->tiles_key)) {
     *ntiles = (long long)c->tiles_h.size();
     return MPROF_OK;
   }
   c->tiles_h.clear();
-  for (long long kb = k_lo; kb < k_hi; kb += kK)
-    for (long long ra = 0; ra < std::min<long long>(L - kb, row_hi); ra += R)
-      c->tiles_h.push_back(make_int2((int)kb, (int)ra));
-  const size_t need = c->tiles_h.size() * sizeof(int2);
+  for (long long kb = k_lo; kb < k_hi; kb += kK) {
+    const long long rend = std::min<long long>(L - kb, row_hi);
+    const long long Rb = block_R(R, std::min<long long>(kK, k_hi - kb), exact);
+    for (long long ra = 0; ra < rend; ra += Rb)
+      c->tiles_h.push_back(make_int4((int)kb, (int)ra, (int)std::min(ra + Rb, rend), 0));
+  }
+  const size_t need = c->tiles_h.size() * sizeof(int4);
   void* p = c->tiles_d;
   int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
-  c->tiles_d = static_cast<int2*>(p);
+  c->tiles_d = static_cast<int4*>(p);
   if (st != MPROF_OK) return st;
   CK(cudaMemcpyAsync(c->tiles_d, c->tiles_h.data(), need, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // tiles_h may be rebuilt by the next call
@@ -667,23 +742,98 @@ constexpr int min_blocks() {
   else return MPROF_MIN_BLOCKS;
 }
 
+// Thresholds from diagonal k1 (FP64 direct evaluation), before the tiles.
 template <class P>
-int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int k1,
-                     bool first_diag, uint32_t* launches, float* ms) {
+int32_t launch_first_diag(mprof_ctx* c, const SweepParams& prm, int k1, uint32_t* launches) {
+  if (k1 > prm.L - 1) return MPROF_OK;
+  k_first_diag<P><<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);
+  CK(cudaGetLastError());
+  ++*launches;
+  return MPROF_OK;
+}
+
+// Tiles [t0, t0 + nt) of the tile table on stream s.
+template <class P>
+int32_t launch_tiles(SweepParams prm, long long t0, long long nt, cudaStream_t s, uint32_t* launches) {
+  if (nt <= 0) return MPROF_OK;
   using SM = SweepSmem<P, kD, kT, kS>;
   const size_t smem = sizeof(SM);
   auto kern = sweep_kernel<P, kD, kT, kS, min_blocks<P>()>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (first_diag && k1 <= prm.L - 1) {
-    k_first_diag<P><<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);
-    CK(cudaGetLastError());
-    ++*launches;
-  }
-  if (ntiles > INT_MAX) return fail(MPROF_E_TOO_LARGE, "too many tiles");
-  if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
-  kern<<<(unsigned)ntiles, kT, smem, c->stream>>>(prm);
+  prm.tiles += t0;
+  kern<<<(unsigned)nt, kT, smem, s>>>(prm);
   CK(cudaGetLastError());
   ++*launches;
+  return MPROF_OK;
+}
+
+// Calls f.template operator()<P>() with the sweep policy of (precision, family, p, exact, filter).
+template <class F>
+int32_t with_policy(const mprof_ctx* c, const mprof_config* cfg, F&& f) {
+  const double p = cfg->p;
+  const bool l2 = cfg->family == MPROF_EUCLIDEAN || (cfg->family == MPROF_PNORM && p == 2.0);
+  if (cfg->precision == MPROF_FP32) {
+    if (cfg->family == MPROF_ZNORMALIZED)
+      return c->zn_colscale ? f.template operator()<ZnormF32<true>>()
+                            : f.template operator()<ZnormF32<false>>();
+    if (l2) return f.template operator()<EuclidF32>();
+    if (p == 1.0) return f.template operator()<PnormF32<1>>();
+    if (p == 3.0) return f.template operator()<PnormF32<3>>();
+    if (p == 4.0) return f.template operator()<PnormF32<4>>();
+    return f.template operator()<PnormF32<0>>();
+  }
+  if (cfg->family == MPROF_ZNORMALIZED)
+    return c->zn_colscale ? f.template operator()<Znorm<true>>() : f.template operator()<Znorm<false>>();
+  const bool ex = cfg->exact != 0;
+  if (l2) return ex ? f.template operator()<Euclid<true>>() : f.template operator()<Euclid<false>>();
+  if (p == 1.0) return ex ? f.template operator()<Pnorm<1, true>>() : f.template operator()<Pnorm<1, false>>();
+  if (p == 3.0) return ex ? f.template operator()<Pnorm<3, true>>() : f.template operator()<Pnorm<3, false>>();
+  if (p == 4.0) return ex ? f.template operator()<Pnorm<4, true>>() : f.template operator()<Pnorm<4, false>>();
+  return ex ? f.template operator()<Pnorm<0, true>>() : f.template operator()<Pnorm<0, false>>();
+}
+
+// Side stream + fork/join events (created on first use).
+int32_t ensure_side(mprof_ctx* c) {
+  if (c->side) return MPROF_OK;
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  return MPROF_OK;
+}
+
+// The sweep of one tile table: optional first-diagonal prepass, then the tiles. Tiles
+// [0, n_near) (the diagonal block next to the exclusion zone) run with the column-scaled z-norm
+// filter on a side stream, concurrently with the rest: there correlations are ~1 and the
+// covariance-only bound (block-wide 1/B extrema) passes nearly every block, whose replays
+// would make those tiles the sweep's critical path.
+int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
+                       long long ntiles, long long n_near, int k1, bool first_diag,
+                       uint32_t* launches, float* ms) {
+  int32_t st = MPROF_OK;
+  if (first_diag && !cfg->exact) {
+    st = with_policy(c, cfg, [&]<class P>() { return launch_first_diag<P>(c, prm, k1, launches); });
+    if (st != MPROF_OK) return st;
+  }
+  if (ntiles > INT_MAX) return fail(MPROF_E_TOO_LARGE, "too many tiles");
+  *ms = 0.f;
+  if (ntiles == 0) return MPROF_OK;
+  if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
+  n_near = std::min(n_near, ntiles);
+  if (n_near > 0) {
+    st = ensure_side(c);
+    if (st != MPROF_OK) return st;
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    st = cfg->precision == MPROF_FP32 ? launch_tiles<ZnormF32<true>>(prm, 0, n_near, c->side, launches)
+                                      : launch_tiles<Znorm<true>>(prm, 0, n_near, c->side, launches);
+    if (st != MPROF_OK) return st;
+    CK(cudaEventRecord(c->ev_join, c->side));
+  }
+  st = with_policy(c, cfg, [&]<class P>() {
+    return launch_tiles<P>(prm, n_near, ntiles - n_near, c->stream, launches);
+  });
+  if (st != MPROF_OK) return st;
+  if (n_near > 0) CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   if (c->timing) {
     CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaEventSynchronize(c->ev1));
@@ -692,41 +842,20 @@ int32_t launch_sweep(mprof_ctx* c, const SweepParams& prm, long long ntiles, int
   return MPROF_OK;
 }
 
-int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
-                       long long ntiles, int k1, uint32_t* launches, float* ms) {
-  const bool fd = !cfg->exact;
-  if (cfg->precision == MPROF_FP32) {
-    if (cfg->family == MPROF_ZNORMALIZED)
-      return c->zn_colscale ? launch_sweep<ZnormF32<true>>(c, prm, ntiles, k1, fd, launches, ms)
-                            : launch_sweep<ZnormF32<false>>(c, prm, ntiles, k1, fd, launches, ms);
-    const double p = cfg->p;
-    if (cfg->family == MPROF_EUCLIDEAN || p == 2.0)
-      return launch_sweep<EuclidF32>(c, prm, ntiles, k1, fd, launches, ms);
-    if (p == 1.0) return launch_sweep<PnormF32<1>>(c, prm, ntiles, k1, fd, launches, ms);
-    if (p == 3.0) return launch_sweep<PnormF32<3>>(c, prm, ntiles, k1, fd, launches, ms);
-    if (p == 4.0) return launch_sweep<PnormF32<4>>(c, prm, ntiles, k1, fd, launches, ms);
-    return launch_sweep<PnormF32<0>>(c, prm, ntiles, k1, fd, launches, ms);
-  }
-  if (cfg->family == MPROF_ZNORMALIZED)
-    return c->zn_colscale ? launch_sweep<Znorm<true>>(c, prm, ntiles, k1, fd, launches, ms)
-                          : launch_sweep<Znorm<false>>(c, prm, ntiles, k1, fd, launches, ms);
-  const bool pn = cfg->family == MPROF_PNORM;
-  const double p = cfg->p;
-  if (!pn || p == 2.0) {
-    return cfg->exact ? launch_sweep<Euclid<true>>(c, prm, ntiles, k1, fd, launches, ms)
-                      : launch_sweep<Euclid<false>>(c, prm, ntiles, k1, fd, launches, ms);
-  }
-  if (p == 1.0)
-    return cfg->exact ? launch_sweep<Pnorm<1, true>>(c, prm, ntiles, k1, fd, launches, ms)
-                      : launch_sweep<Pnorm<1, false>>(c, prm, ntiles, k1, fd, launches, ms);
-  if (p == 3.0)
-    return cfg->exact ? launch_sweep<Pnorm<3, true>>(c, prm, ntiles, k1, fd, launches, ms)
-                      : launch_sweep<Pnorm<3, false>>(c, prm, ntiles, k1, fd, launches, ms);
-  if (p == 4.0)
-    return cfg->exact ? launch_sweep<Pnorm<4, true>>(c, prm, ntiles, k1, fd, launches, ms)
-                      : launch_sweep<Pnorm<4, false>>(c, prm, ntiles, k1, fd, launches, ms);
-  return cfg->exact ? launch_sweep<Pnorm<0, true>>(c, prm, ntiles, k1, fd, launches, ms)
-                    : launch_sweep<Pnorm<0, false>>(c, prm, ntiles, k1, fd, launches, ms);
+// Resident sweep CTAs per SM of the policy's kernel (registers + shared memory), >= 1.
+int sweep_blocks_per_sm(const mprof_ctx* c, const mprof_config* cfg) {
+  int nb = 1;
+  with_policy(c, cfg, [&]<class P>() {
+    using SM = SweepSmem<P, kD, kT, kS>;
+    auto kern = sweep_kernel<P, kD, kT, kS, min_blocks<P>()>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SM)) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kT, sizeof(SM)) != cudaSuccess)
+      nb = 1;
+    cudaGetLastError();
+    return 0;
+  });
+  return std::max(1, nb);
 }
 
 int32_t check_config(uint64_t n, const mprof_config* cfg) {
@@ -817,14 +946,22 @@ struct SweepOut {
   long long ntiles = 0, R = 0;
 };
 
+// first_diag: seed the filter thresholds with diagonal `exclusion` (evaluated directly). Those are
+// genuine cells even when the band starts further out, so band profiles still merge exactly, and
+// every band starts from near-final thresholds (random walks: ~all nearest neighbours at k = 1).
 int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
-                    const Workspace& w, int k_lo, int k_hi, int row_hi, int rl, uint32_t* launches,
-                    SweepOut* out) {
+                    const Workspace& w, int k_lo, int k_hi, int row_hi, int rl, bool first_diag,
+                    uint32_t* launches, SweepOut* out) {
   const int m = (int)cfg->m;
   const int L = n - m + 1;
   if (k_lo >= k_hi || row_hi <= 0) return MPROF_OK;
-  out->R = choose_R(cfg, L, k_lo, k_hi, row_hi, c->num_sms);
-  int32_t st = build_tiles(c, L, k_lo, k_hi, row_hi, out->R, &out->ntiles);
+  first_diag = first_diag && !cfg->exact;
+  // Diagonal `exclusion` is evaluated directly by the prepass; sweeping it again in the tiles
+  // would re-offer values equal to the thresholds they set (every block of those lanes replays
+  // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
+  const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
+  out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg));
+  int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, &out->ntiles);
   if (st != MPROF_OK) return st;
   SweepParams prm;
   prm.t = d_t;
@@ -849,7 +986,12 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
   }
-  st = dispatch_sweep(c, cfg, prm, out->ntiles, k_lo, launches, &out->ms);
+  long long n_near = 0;
+  if (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale && !cfg->exact &&
+      k_tile <= (int)cfg->exclusion + 1 && !getenv("MPROF_ZN_NO_NEAR"))
+    n_near = count_tiles(L, k_tile, std::min(k_tile + kK, k_hi), row_hi, out->R);  // first block
+  st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
+                      &out->ms);
   if (st != MPROF_OK) return st;
   if (want_stats) {
     unsigned long long h[2];
@@ -927,7 +1069,7 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   SweepOut so;
   long long k_done = k_hi;
   if (!c->progress || k_lo >= k_hi) {
-    st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, 0, &launches, &so);
+    st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, 0, true, &launches, &so);
     if (st != MPROF_OK) return st;
   } else {
     // Anytime mode (scan_diagonals' observer, /root/reference/proj/src/detail/diag_scan.hpp:
@@ -939,7 +1081,7 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     for (long long a = k_lo; a < k_hi; a += chunk) {
       const long long b = std::min(k_hi, a + chunk);
       SweepOut part;
-      st = sweep_tiles(c, d_t, n, cfg, w, (int)a, (int)b, L, 0, &launches, &part);
+      st = sweep_tiles(c, d_t, n, cfg, w, (int)a, (int)b, L, 0, a == k_lo, &launches, &part);
       if (st != MPROF_OK) return st;
       so.ms += part.ms;
       so.ntiles += part.ntiles;
@@ -1088,6 +1230,12 @@ void mprof_ctx_destroy(mprof_ctx* c) {
   if (c->d_spread) cudaFree(c->d_spread);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+  }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   for (auto it = g_default_ctx.begin(); it != g_default_ctx.end(); ++it)
     if (it->second == c) { g_default_ctx.erase(it); break; }
@@ -1162,9 +1310,37 @@ int32_t mprof_finalize_device(mprof_ctx* in, const double* d_t, uint64_t n, cons
     st = ensure_znorm_stats(c, d_t, n, cfg, w);
     if (st != MPROF_OK) return st;
   }
-  k_finalize<<<grid_for(32LL * L), 256, 0, c->stream>>>(d_t, d_cmp, d_idx, w.mu, w.B, d_P, L,
-                                                          (int)cfg->m, cfg->family, cfg->p,
-                                                          cfg->exact ? 1 : 0);
+  k_finalize_range<<<grid_for(32LL * L), 256, 0, c->stream>>>(d_t, d_cmp, d_idx, w.mu, w.B, d_P, 0, L,
+                                                                (int)cfg->m, cfg->family, cfg->p,
+                                                                cfg->exact ? 1 : 0);
+  CK(cudaGetLastError());
+  return MPROF_OK;
+}
+
+int32_t mprof_finalize_range_device(mprof_ctx* in, const double* d_t, uint64_t n,
+                                    const double* d_cmp, const int64_t* d_idx,
+                                    const mprof_config* cfg, double* d_P, uint64_t lo,
+                                    uint64_t hi) {
+  if (!d_t || !d_cmp || !d_idx || !cfg || !d_P) return fail(MPROF_E_BAD_ARG, "null argument");
+  int32_t st = check_config(n, cfg);
+  if (st != MPROF_OK) return st;
+  const uint64_t L = n - cfg->m + 1;
+  if (hi > L) hi = L;
+  if (lo >= hi) return MPROF_OK;
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  Workspace w;
+  st = carve(c, (int)L, &w);
+  if (st != MPROF_OK) return st;
+  if (cfg->family == MPROF_ZNORMALIZED) {
+    st = ensure_znorm_stats(c, d_t, n, cfg, w);
+    if (st != MPROF_OK) return st;
+  }
+  // entries [lo, hi): shift the per-entry arrays; the series / statistics stay absolute
+  k_finalize_range<<<grid_for(32LL * (long long)(hi - lo)), 256, 0, c->stream>>>(
+      d_t, d_cmp, d_idx, w.mu, w.B, d_P, (int)lo, (int)hi, (int)cfg->m, cfg->family, cfg->p,
+      cfg->exact ? 1 : 0);
   CK(cudaGetLastError());
   return MPROF_OK;
 }
@@ -1206,6 +1382,13 @@ int32_t mprof_band_cuts(uint64_t n, uint64_t m, uint64_t exclusion, uint32_t par
     while (a < b) {
       const uint64_t mid = a + (b - a) / 2;
       if ((long double)mprof_band_cells(n, m, exclusion, mid) >= target) b = mid; else a = mid + 1;
+    }
+    // align to whole diagonal blocks of the tile grid (first tile diagonal exclusion + 1, the
+    // prepass sweeps `exclusion`): a band's last block would otherwise be a thin, slow tile row
+    const uint64_t base = exclusion + 1;
+    if (a > base && a < L) {
+      const uint64_t q = (a - base + kK / 2) / kK;
+      a = std::min<uint64_t>(L, std::max<uint64_t>(lo, base + q * kK));
     }
     cuts[g] = a;
     lo = a;
@@ -1294,7 +1477,7 @@ int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count
   ++launches;
   SweepOut so;
   const int k_lo = (int)cfg->exclusion;
-  st = sweep_tiles(c, S->rev, (int)n_new, cfg, w, k_lo, L_new, dL, L_new, &launches, &so);
+  st = sweep_tiles(c, S->rev, (int)n_new, cfg, w, k_lo, L_new, dL, L_new, true, &launches, &so);
   if (st != MPROF_OK) return st;
   BestEntry* fwd = static_cast<BestEntry*>(S->fwd);
   k_unreverse<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, fwd, L_new);

@@ -352,7 +352,7 @@ struct SweepParams {
   const float* B32;       // FP32 mode scales
   const double* mu;       // window means (z-norm), valid [0, L)
   BestEntry* best;        // L entries
-  const int2* tiles;      // (first diagonal kb, first row ra) per CTA
+  const int4* tiles;      // (first diagonal kb, first row ra, row end re, -) per CTA
   int n, m, L;
   int k_hi;               // exclusive upper bound of the swept diagonal band
   int R;                  // rows per tile
@@ -723,13 +723,13 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
-  const int2 tl = prm.tiles[blockIdx.x];
+  const int4 tl = prm.tiles[blockIdx.x];
   const int kb = tl.x, ra = tl.y;
+  const int re = tl.z;  // exclusive row end of the tile (<= L - kb, <= row_hi)
   const int L = prm.L;
   const int m = prm.m;
   const int kt = kb + static_cast<int>(threadIdx.x) * D;
   const int kend = min(kb + G::K, prm.k_hi);
-  const int re = min(min(ra + prm.R, L - kb), prm.row_hi);  // exclusive row end of the tile
 
   // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d) --------------------
   double sacc[D];

@@ -70,3 +70,28 @@ def test_band_partition_covers_every_diagonal_once():
         bands = [band_for_rank(n, m, excl, r, world) for r in range(world)]
         assert bands[0][0] == excl and bands[-1][1] == n - m + 1
         assert all(a[1] == b[0] for a, b in zip(bands[:-1], bands[1:]))
+
+
+def _gather_worker(rank, world, port, L, out_dir):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_1901_05708_b200.distributed import gather_shards_, shard_range, shard_size
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = torch.full((world * shard_size(L, world),), -1.0, dtype=torch.float64)
+    lo, hi = shard_range(L, rank, world)
+    x[lo:hi] = torch.arange(lo, hi, dtype=torch.float64) * 0.5  # this rank's finalized slice
+    gather_shards_(x)
+    np.save(os.path.join(out_dir, f"x{rank}.npy"), x[:L].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,L", [(2, 7), (3, 10), (3, 3), (4, 2)])
+def test_sharded_finalize_gather(tmp_path, world, L):
+    """Range-split finalize: every rank ends with all L entries, each written by its owner."""
+    tmp.spawn(_gather_worker, args=(world, _free_port(), L, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"x{r}.npy"), np.arange(L) * 0.5)

@@ -316,6 +316,13 @@ def test_bands_merge_to_full_profile(mp):
     mp.finalize_device(d_t.data_ptr(), t.size, d_cm.data_ptr(), d_im.data_ptr(), cfg, P.data_ptr())
     torch.cuda.synchronize()
     assert_parity(t, m, ZNORM, 2.0, P.cpu().numpy(), im, Pr, Ir)
+    # range-split finalize (multi-GPU: each rank converts its own slice) == whole finalize
+    P2 = torch.full((L,), -7.0, dtype=torch.float64, device="cuda")
+    for lo in range(0, L, 3001):
+        mp.finalize_range_device(d_t.data_ptr(), t.size, d_cm.data_ptr(), d_im.data_ptr(), cfg,
+                                 P2.data_ptr(), lo, min(L, lo + 3001))
+    torch.cuda.synchronize()
+    assert torch.equal(P, P2)
 
 
 def test_fp64_peak_is_plausible(mp):

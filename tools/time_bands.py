@@ -1,0 +1,40 @@
+"""Per-band sweep times of the C4 engines when the diagonals are split into `world` equal-area
+bands (what each rank of a world-GPU run sweeps), timed one band at a time on one GPU.
+max over bands ~ the multi-GPU sweep time; experiments only."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1901_05708_b200 as mp  # noqa: E402
+from paper_1901_05708_b200 import workloads as W  # noqa: E402
+
+worlds = [int(x) for x in (sys.argv[1:] or ["1", "2", "4", "8"])]
+ctx = mp.Context(0)
+ctx.set_timing(True)
+t = W.c4()
+n, m = t.size, 1024
+L = n - m + 1
+d_t = torch.tensor(t, dtype=torch.float64, device="cuda")
+cmp = torch.empty(L, dtype=torch.float64, device="cuda")
+idx = torch.empty(L, dtype=torch.int64, device="cuda")
+torch.cuda.synchronize()
+out = {}
+for fam, kind in (("aamp", mp.DistanceKind.euclidean()), ("acamp", mp.DistanceKind.znormalized())):
+    cfg = mp.ProfileConfig(m, kind)
+    for world in worlds:
+        cuts = mp.band_cuts(n, m, 1, world)
+        ms, Rs = [], []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            best = 1e30
+            for _ in range(3):
+                info = mp.sweep_device(d_t.data_ptr(), n, cfg, a, b, cmp.data_ptr(), idx.data_ptr(),
+                                       ctx=ctx)
+                best = min(best, info.sweep_ms)
+            ms.append(round(best, 3))
+            Rs.append(info.rows_per_tile)
+        out[f"{fam}_w{world}"] = {"band_ms": ms, "max": max(ms), "sum": round(sum(ms), 3), "R": Rs}
+        print(fam, world, out[f"{fam}_w{world}"], flush=True)
+print(json.dumps(out))
