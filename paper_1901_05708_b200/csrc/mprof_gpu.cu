@@ -500,6 +500,8 @@ struct mprof_ctx {
   int4* tiles_d = nullptr;
   size_t tiles_cap = 0;
   long long tiles_key[6] = {-1, -1, -1, -1, -1, -1};
+  long long R_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // rows-per-tile choice cache
+  long long R_val = 0;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
   const double* stats_t = nullptr;
   uint64_t stats_n = 0, stats_m = 0;
@@ -676,7 +678,8 @@ double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int
 // Rows per tile. Longest runs amortise the seeds best (R_max = 32 m rows), but a grid of a few
 // waves loses up to a whole wave to its tail: the candidates R_max / j (stage multiples) are
 // scheduled on the sweep kernel's real residency (slots = occupancy x SMs) and the shortest
-// makespan wins (ties -> longer tiles). Grids beyond 48 waves keep R_max.
+// makespan wins (ties -> longer tiles). Grids of >= 16 waves keep R_max (tail < ~3 %). The
+// choice is cached per context and shape (the simulation costs up to a few ms of host time).
 long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int slots) {
   if (cfg->exact) {
     if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
@@ -687,14 +690,14 @@ long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_h
   if (cfg->refresh_interval > 0) Rmax = std::min<long long>(Rmax, (long long)cfg->refresh_interval);
   long long R = Rmax;
   if (const char* e = getenv("MPROF_ROWS_PER_TILE")) return std::max(1LL, atoll(e));  // experiments
-  if (Rmax > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, Rmax) < 48LL * slots) {
+  if (Rmax > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, Rmax) < 16LL * slots) {
     double best = schedule_makespan(L, k_lo, k_hi, row_hi, Rmax, slots, (int)cfg->m);
     long long prev = Rmax;
-    for (int j = 2; j <= 64; ++j) {
+    for (int j = 2; j <= 32; ++j) {
       const long long Rj = std::max<long long>(2 * kS, (Rmax / j + kS - 1) / kS * kS);
       if (Rj >= prev) continue;
       prev = Rj;
-      if (count_tiles(L, k_lo, k_hi, row_hi, Rj) > 256LL * slots) break;
+      if (count_tiles(L, k_lo, k_hi, row_hi, Rj) > 32LL * slots) break;
       const double ms = schedule_makespan(L, k_lo, k_hi, row_hi, Rj, slots, (int)cfg->m);
       if (getenv("MPROF_TILE_DEBUG"))
         fprintf(stderr, "[mprof tiles] slots %d R %lld tiles %lld makespan %.0f (R_max %.0f)\n", slots,
@@ -960,7 +963,23 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   // would re-offer values equal to the thresholds they set (every block of those lanes replays
   // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
   const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
-  out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg));
+  {
+    long long pbits;
+    std::memcpy(&pbits, &cfg->p, sizeof pbits);
+    const long long key[9] = {L, k_tile, k_hi, row_hi, (long long)cfg->m, cfg->exact,
+                              (long long)cfg->refresh_interval,
+                              ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0),
+                              pbits};
+    if (std::equal(key, key + 9, c->R_key)) {
+      out->R = c->R_val;
+    } else {
+      out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg));
+      if (!getenv("MPROF_ROWS_PER_TILE")) {
+        std::copy(key, key + 9, c->R_key);
+        c->R_val = out->R;
+      }
+    }
+  }
   int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, &out->ntiles);
   if (st != MPROF_OK) return st;
   SweepParams prm;

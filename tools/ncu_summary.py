@@ -52,14 +52,17 @@ def launches(path: Path, tag: str):
     print("\n".join(out))
 
 
-def full(rep: Path, tag: str):
+def _rows(rep: Path):
     raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    h, units = rows[0], rows[1]
+    return rows[0], rows[1], rows[2:]
+
+
+def full(reps, tag: str):
     summary = {}
-    lines = [f"# ncu --set full summary ({rep.name})"]
-    for r in rows[2:]:
+    lines = [f"# ncu --set full summary ({', '.join(r.name for r in reps)})"]
+    for h, units, r in ((h, u, r) for rep in reps for h, u, rs in [_rows(rep)] for r in rs):
         name = r[h.index("Kernel Name")]
         d = {}
         for k in KEYS:
@@ -100,9 +103,10 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
     ap.add_argument("--launches", default=str(ROOT / "gpurun_out" / "launches.csv"))
-    ap.add_argument("--rep", default=str(ROOT / "gpurun_out" / "prof.ncu-rep"))
+    ap.add_argument("--rep", action="append", default=None, help="repeatable")
     a = ap.parse_args()
     if Path(a.launches).exists():
         launches(Path(a.launches), a.tag)
-    if Path(a.rep).exists():
-        full(Path(a.rep), a.tag)
+    reps = [Path(r) for r in (a.rep or [str(ROOT / "gpurun_out" / "prof.ncu-rep")]) if Path(r).exists()]
+    if reps:
+        full(reps, a.tag)
