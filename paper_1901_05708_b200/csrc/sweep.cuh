@@ -81,6 +81,11 @@ struct KeyF64 {
   // covariance-filter key and bound (larger covariance = better): ~hi is decreasing
   __device__ __forceinline__ static int cov_key(double c) { return ~__double2hiint(c); }
   __device__ __forceinline__ static int cov_bound(double th) { return ~__double2hiint(th); }
+  // covariance-only form in raw (order-preserving) words: hit <=> max raw(cov) >= raw bound
+  __device__ __forceinline__ static int cov_raw(double c) { return __double2hiint(c); }
+  __device__ __forceinline__ static int cov_bound_raw_f(float th) {  // th > 0, exact in double
+    return __double2hiint(static_cast<double>(th));
+  }
 };
 struct KeyF32 {
   __device__ __forceinline__ static int key(float v) { return __float_as_int(v); }
@@ -92,6 +97,8 @@ struct KeyF32 {
   __device__ __forceinline__ static int cov_bound(double th) {
     return ~__float_as_int(__double2float_rd(th));
   }
+  __device__ __forceinline__ static int cov_raw(float c) { return __float_as_int(c); }
+  __device__ __forceinline__ static int cov_bound_raw_f(float th) { return __float_as_int(th); }
 };
 
 // AAMP. Reference: incremental_euclidean_step (/root/reference/proj/include/mprof/aamp.hpp:37-42),
@@ -331,17 +338,21 @@ struct SweepSmem {
   V2 colA[G::RINGP];                           // ring: A[cbase + X] at pad(X mod RING)
   VB colB[HASB ? G::RINGP : 2];                // ring: B[cbase + 1 + X]
   int colT[2][G::NCOLP];                       // hi32(best[i0 + kb + 1 + x].v), exact
-  int colBM[2][NCB];                           // max of colT over aligned blocks of D
+  int colBM2[2][NCB];                          // max of colT over columns [cD, cD + 2D)
   V2 rowA[2][S];                               // A[i0 + x]
   VB rowB[2][HASB ? S : 2];                    // B[i0 + 1 + x]
   int rowT[2][S];                              // hi32(best[i0 + 1 + x].v), exact
   int rowBM[2][S / D];                         // max of rowT over aligned blocks of D
-  // z-norm filter scales, rounded DOWN (a smaller scale only loosens the filter): per aligned
-  // block of D columns in a ring of RING/D blocks (filled once, when the block arrives), per
-  // block of D rows and per row of the stage.
-  float colIB[HASB ? G::RING / D : 1];         // <= 1 / max colB of the block
-  float rowIB[2][HASB ? S / D : 1];            // <= 1 / max rowB of the block
-  float rowIBx[2][HASB ? S : 1];               // <= 1 / rowB of each row
+  // z-norm filter scales, rounded DOWN (a smaller scale only loosens the filter).
+  float rowIBx[2][HASB ? S : 1];               // <= 1 / rowB of each row (column-scaled form)
+  // Covariance-only z-norm filter, per stage: for row block r, {lower bound of (1 - tau_r) *
+  // IB_r, IB_r}; for column block c (covering stage columns [cD, cD + 2D)), {lower bound of
+  // (1 - tau_c) * IB_c, IB_c}, tau = max threshold, IB <= 1 / max B of the block; -inf = "some
+  // threshold >= 1, every cell may pass". A block's covariance bound is then
+  // min(RQ_r * IB_c, CQ_c * IB_r) (= (1 - max(tau_r, tau_c)) * IB_r * IB_c).
+  static constexpr bool ZQ = P::kCovFilter && !P::kColScale;
+  float2 zrow[2][ZQ ? S / D : 1];
+  float2 zcol[2][ZQ ? NCB : 1];
 };
 
 struct SweepParams {
@@ -537,30 +548,34 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
     }
   }
   const V2* rowA = sm.rowA[b];
-  // Block threshold (software-pipelined: block s+D's is computed at the start of block s, so its
-  // shared-load -> convert -> multiply chain overlaps the block's FP64 work).
+  // Block threshold (software-pipelined: block s+D's is computed during block s, unconditionally
+  // with a clamped index, so its shared-load -> convert -> multiply chain overlaps the block's
+  // FP64 work instead of sitting between the block's hit test and the next block).
   // theta: key bound of the block; num: covariance filters' 1 - tau_max (0 = every cell may pass)
   auto block_theta = [&](int s, int& theta, double& num) {
     const int cb = s / D + threadIdx.x;
-    const int tmax = max(sm.rowBM[b][s / D], max(sm.colBM[b][cb], sm.colBM[b][cb + 1]));
+    const int tmax = max(sm.rowBM[b][s / D], sm.colBM2[b][cb]);
     theta = P::tau(tmax);
     num = 0.0;
-    if constexpr (P::kCovFilter) {
-      if (tmax >= 0x3FF00000) {
-        theta = INT_MAX;  // some threshold >= 1: any cell may qualify
-      } else {
-        num = (1.0 - __hiloint2double(tmax, -1)) * (1.0 - 0x1p-40);  // margin for roundings
-        if constexpr (!kColScale) {
-          const int cq = (X0 / D + cb) % (G::RING / D);
-          const float ic = fminf(sm.colIB[cq], sm.colIB[cq + 1 == G::RING / D ? 0 : cq + 1]);
-          theta = P::cov_bound(num * static_cast<double>(sm.rowIB[b][s / D]) * static_cast<double>(ic));
-        }
-      }
+    if constexpr (P::kCovFilter && kColScale) {
+      if (tmax >= 0x3FF00000) theta = INT_MAX;  // some threshold >= 1: any cell may qualify
+      else num = (1.0 - __hiloint2double(tmax, -1)) * (1.0 - 0x1p-40);  // margin for roundings
     }
   };
+  // Covariance-only form: the stage tables make it two broadcast/strided loads and float math;
+  // the bound is kept as a raw word (hit <=> max raw(cov) >= bound), INT_MIN = every cell may
+  // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
+  constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ;
+  auto block_theta_cov = [&](int s) {
+    const float2 rq = sm.zrow[b][s / D];
+    const float2 cq = sm.zcol[b][s / D + threadIdx.x];
+    const float th = fminf(__fmul_rd(rq.x, cq.y), __fmul_rd(cq.x, rq.y));
+    return th > 0.f ? P::cov_bound_raw_f(th) : INT_MIN;
+  };
   int theta_nx;
-  double num_nx;
-  block_theta(0, theta_nx, num_nx);
+  double num_nx = 0.0;
+  if constexpr (ZQ) theta_nx = block_theta_cov(0);
+  else block_theta(0, theta_nx, num_nx);
   for (int s = 0; s < cnt; s += D) {
     // the D operands entering during this block are contiguous in the ring: constant offsets
     const int qn = G::pad((X0 + s + xb + D) % G::RING);
@@ -568,11 +583,12 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
     const VB* nB = &sm.colB[P::kHasB ? qn : 0];
     const int theta = theta_nx;
     const double num = num_nx;
-    if (s + D < cnt) block_theta(s + D, theta_nx, num_nx);
+    if constexpr (ZQ) theta_nx = block_theta_cov(min(s + D, S - D));
+    else block_theta(min(s + D, S - D), theta_nx, num_nx);
     Acc<P, D> acc0;
 #pragma unroll
     for (int d = 0; d < D; ++d) acc0.a[d] = acc[d];
-    int hmin = INT_MAX;
+    int hmin = ZQ ? INT_MIN : INT_MAX;  // ZQ: running MAX of raw covariance words
     bool hit = false;
 #pragma unroll
     for (int u = 0; u < D; ++u) {
@@ -580,23 +596,30 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       const int x = s + u;
       const V2 r = rowA[x];
       const int row = i0 + x + 1;
-      int hu = INT_MAX;
+      int hu = ZQ ? INT_MIN : INT_MAX;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int sl = (d + u) % D;
         acc[d] = P::step(acc[d], r, cA[sl], p);
-        int h;
-        if constexpr (kColScale) h = P::cov_key(acc[d] * cB[sl]);
-        else if constexpr (P::kCovFilter) h = P::cov_key(acc[d]);
-        else h = P::key(acc[d]);
-        if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
-        hu = min(hu, h);
+        if constexpr (ZQ) {
+          int h = P::cov_raw(acc[d]);
+          if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MIN;
+          hu = max(hu, h);
+        } else {
+          int h;
+          if constexpr (kColScale) h = P::cov_key(acc[d] * cB[sl]);
+          else h = P::key(acc[d]);
+          if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
+          hu = min(hu, h);
+        }
       }
       if constexpr (kColScale) {
         // row bound for this sub-step: cov * B_j >= (1 - tau) / B_i
         const int tu = (num == 0.0) ? INT_MAX
                                     : P::cov_bound(num * static_cast<double>(sm.rowIBx[b][x]));
         hit |= hu <= tu;
+      } else if constexpr (ZQ) {
+        hmin = max(hmin, hu);
       } else {
         hmin = min(hmin, hu);
       }
@@ -604,7 +627,8 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       cA[u] = nA[u];
       if constexpr (kColScale) cB[u] = nB[u];
     }
-    if constexpr (!kColScale) hit = hmin <= theta;
+    if constexpr (ZQ) hit = hmin >= theta;
+    else if constexpr (!kColScale) hit = hmin <= theta;
     if (hit) {
       const int q1 = G::pad((X0 + s + xb) % G::RING);
       const int q2 = G::pad((X0 + s + xb + D) % G::RING);
@@ -630,20 +654,30 @@ __device__ __forceinline__ float inv_bound(int w) {
   else return __frcp_rd(__int_as_float(w));
 }
 
+// Lower bound of (1 - tau) * ib, tau <= the largest value with high word tmax; -inf when tau may
+// reach 1 (every cell may qualify) or the bound underflows.
+__device__ __forceinline__ float one_minus_tau_ib(int tmax, float ib) {
+  if (tmax >= 0x3FF00000) return -INFINITY;
+  const float u = __double2float_rd((1.0 - __hiloint2double(tmax, -1)) * (1.0 - 0x1p-40));
+  return u > 0.f ? __fmul_rd(u, ib) : -INFINITY;
+}
+
 // Block maxima of the freshly loaded thresholds (after the stage's cp.async completed).
 template <class P, int D, int T, int S>
 __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b, int X0) {
   using G = Geo<D, T, S>;
   using SM = SweepSmem<P, D, T, S>;
   using VB = typename P::VB;
-  for (int blk = threadIdx.x; blk < SM::NCB; blk += T) {
+  // the columns one thread's block touches are [cD, cD + 2D - 1): two aligned blocks, read from
+  // the raw words (no dependency on other threads' results of this call)
+  for (int blk = threadIdx.x; blk < SM::NCB - 1; blk += T) {
     int mx = INT_MIN;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
+    for (int d = 0; d < 2 * D; ++d) {
       const int x = blk * D + d;
       if (x < G::NCOL) mx = max(mx, sm.colT[b][G::pad(x)]);
     }
-    sm.colBM[b][blk] = mx;
+    sm.colBM2[b][blk] = mx;
   }
   for (int blk = threadIdx.x; blk < S / D; blk += T) {
     int mx = INT_MIN;
@@ -651,23 +685,34 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
     for (int d = 0; d < D; ++d) mx = max(mx, sm.rowT[b][blk * D + d]);
     sm.rowBM[b][blk] = mx;
   }
-  if constexpr (P::kHasB) {
-    const int first = (X0 == 0) ? 0 : (X0 + G::K) / D;  // column blocks that arrived for this stage
-    const int last = (X0 + G::NCOL) / D;
-    for (int bx = first + static_cast<int>(threadIdx.x); bx < last; bx += T) {
-      const int q = G::pad((bx * D) % G::RING);
-      int hmax = 0;
-#pragma unroll
-      for (int d = 0; d < D; ++d) hmax = max(hmax, scale_word<VB>(&sm.colB[q + d]));
-      sm.colIB[bx % (G::RING / D)] = inv_bound<VB>(hmax);
-    }
+  if constexpr (P::kColScale) {
     for (int x = threadIdx.x; x < S; x += T)
       sm.rowIBx[b][x] = inv_bound<VB>(scale_word<VB>(&sm.rowB[b][x]));
+  }
+  if constexpr (SM::ZQ) {
     for (int blk = threadIdx.x; blk < S / D; blk += T) {
       int hmax = 0;
 #pragma unroll
       for (int d = 0; d < D; ++d) hmax = max(hmax, scale_word<VB>(&sm.rowB[b][blk * D + d]));
-      sm.rowIB[b][blk] = inv_bound<VB>(hmax);
+      const float ib = inv_bound<VB>(hmax);
+      sm.zrow[b][blk] = make_float2(one_minus_tau_ib(sm.rowBM[b][blk], ib), ib);  // same thread wrote rowBM
+    }
+    {
+      // column blocks c = 0 .. NCB-2 of the stage, each over its two aligned D-blocks (the
+      // columns [cD, cD + 2D - 1) one thread's block touches), from the raw words: no dependency
+      // on other threads. results of this call
+      for (int c = threadIdx.x; c < SM::NCB - 1; c += T) {
+        int hmax = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int q = G::pad((X0 + (c + h) * D) % G::RING);
+#pragma unroll
+          for (int d = 0; d < D; ++d)
+            if ((c + h) * D + d < G::NCOL) hmax = max(hmax, scale_word<VB>(&sm.colB[q + d]));
+        }
+        const float ib = inv_bound<VB>(hmax);
+        sm.zcol[b][c] = make_float2(one_minus_tau_ib(sm.colBM2[b][c], ib), ib);  // same thread
+      }
     }
   }
 }
