@@ -11,25 +11,31 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1901_05708_b200 as mp  # noqa: E402
 from paper_1901_05708_b200 import workloads as W  # noqa: E402
 
-worlds = [int(x) for x in (sys.argv[1:] or ["1", "2", "4", "8"])]
+args = sys.argv[1:]
+cfg_name = args.pop(0) if args and not args[0].isdigit() else "C4"  # C4 (both engines) or C5
+worlds = [int(x) for x in (args or ["1", "2", "4", "8"])]
 ctx = mp.Context(0)
 ctx.set_timing(True)
-t = W.c4()
-n, m = t.size, 1024
+c = W.CONFIGS["C4aamp" if cfg_name == "C4" else cfg_name]
+t = c.gen()
+n, m = t.size, c.m
 L = n - m + 1
 d_t = torch.tensor(t, dtype=torch.float64, device="cuda")
 cmp = torch.empty(L, dtype=torch.float64, device="cuda")
 idx = torch.empty(L, dtype=torch.int64, device="cuda")
 torch.cuda.synchronize()
 out = {}
-for fam, kind in (("aamp", mp.DistanceKind.euclidean()), ("acamp", mp.DistanceKind.znormalized())):
+engines = (("aamp", mp.DistanceKind.euclidean()), ("acamp", mp.DistanceKind.znormalized()))
+if cfg_name != "C4":
+    engines = engines[1:]  # C5: ACAMP
+for fam, kind in engines:
     cfg = mp.ProfileConfig(m, kind)
     for world in worlds:
         cuts = mp.band_cuts(n, m, 1, world)
         ms, Rs = [], []
         for a, b in zip(cuts[:-1], cuts[1:]):
             best = 1e30
-            for _ in range(3):
+            for _ in range(3 if cfg_name == "C4" else 1):
                 info = mp.sweep_device(d_t.data_ptr(), n, cfg, a, b, cmp.data_ptr(), idx.data_ptr(),
                                        ctx=ctx)
                 best = min(best, info.sweep_ms)
