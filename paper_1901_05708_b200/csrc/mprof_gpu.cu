@@ -499,7 +499,7 @@ struct mprof_ctx {
   std::vector<int4> tiles_h;  // (first diagonal, first row, row end, -)
   int4* tiles_d = nullptr;
   size_t tiles_cap = 0;
-  long long tiles_key[6] = {-1, -1, -1, -1, -1, -1};
+  long long tiles_key[7] = {-1, -1, -1, -1, -1, -1, -1};
   long long R_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // rows-per-tile choice cache
   long long R_val = 0;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
@@ -650,27 +650,61 @@ double tile_cells(long long L, long long kb, long long k_hi, long long row_hi, l
   return full + tri;
 }
 
-// Makespan (in row-steps of a full-width tile) of the tile list in launch order on `slots`
-// resident CTAs: the block scheduler hands the next tile to the first free slot (list
-// scheduling). Per-tile fixed cost: the FP64 seeds (m per diagonal, ~1/3 of a row-step each in
-// FP64-pipe terms) plus pipeline fill.
-double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int slots, int m) {
-  std::vector<double> heap(slots, 0.0);  // min-heap of slot free times
-  auto cmp = std::greater<double>();
+// The tile table in launch order, with each tile's modelled cost (row-steps of a full-width
+// tile: cells / K, with a per-row latency floor of a quarter row-step for narrow tiles, plus the
+// FP64 seeds, m per diagonal ~ 1/3 row-step each in FP64-pipe terms, and pipeline fill), in
+// diagonal-block order; the first block's tiles come first (they may run on the near-diagonal
+// side stream, dispatch_sweep). Longest-first ordering of the partial tiles was measured: +1 %
+// on C4 AAMP, -11 % on C3 (MPROF_TILE_ORDER_LPT keeps it available for experiments).
+void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, int m,
+               std::vector<int4>& tiles, std::vector<double>* costs) {
+  tiles.clear();
+  std::vector<double> cost;
   const double fixed = (double)m / 3.0 + 2.0 * kS;
-  double makespan = 0.0;
+  size_t first_block = 0;
   for (long long kb = k_lo; kb < k_hi; kb += kK) {
     const long long w = std::min<long long>(kK, k_hi - kb);
-    const long long Rb = block_R(R, w, false);
-    for (long long ra = 0; ra < std::min<long long>(L - kb, row_hi); ra += Rb) {
-      std::pop_heap(heap.begin(), heap.end(), cmp);
-      // narrow tiles: per-row latency floor of a quarter of a full row-step
+    const long long rend = std::min<long long>(L - kb, row_hi);
+    const long long Rb = block_R(R, w, exact);
+    for (long long ra = 0; ra < rend; ra += Rb) {
+      tiles.push_back(make_int4((int)kb, (int)ra, (int)std::min(ra + Rb, rend), 0));
       const double cells = tile_cells(L, kb, k_hi, row_hi, ra, Rb);
-      const double end = heap.back() + std::max(cells / kK, cells / w * 0.25) + fixed;
-      heap.back() = end;
-      std::push_heap(heap.begin(), heap.end(), cmp);
-      makespan = std::max(makespan, end);
+      cost.push_back(std::max(cells / kK, cells / w * 0.25) + fixed);
     }
+    if (kb == k_lo) first_block = tiles.size();
+  }
+  if (getenv("MPROF_TILE_ORDER_LPT")) {  // experiments: decreasing cost after the first block
+    std::vector<size_t> ord(tiles.size());
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+    std::stable_sort(ord.begin() + first_block, ord.end(),
+                     [&](size_t x, size_t y) { return cost[x] > cost[y]; });
+    std::vector<int4> sorted(tiles.size());
+    std::vector<double> sorted_cost(tiles.size());
+    for (size_t i = 0; i < ord.size(); ++i) {
+      sorted[i] = tiles[ord[i]];
+      sorted_cost[i] = cost[ord[i]];
+    }
+    tiles.swap(sorted);
+    cost.swap(sorted_cost);
+  }
+  if (costs) costs->swap(cost);
+}
+
+// Makespan (in row-steps of a full-width tile) of the tile list in launch order on `slots`
+// resident CTAs: the block scheduler hands the next tile to the first free slot (list
+// scheduling).
+double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int slots, int m) {
+  std::vector<int4> tiles;
+  std::vector<double> cost;
+  tile_list(L, k_lo, k_hi, row_hi, R, false, m, tiles, &cost);
+  std::vector<double> heap(slots, 0.0);  // min-heap of slot free times
+  auto cmp = std::greater<double>();
+  double makespan = 0.0;
+  for (double c : cost) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    heap.back() += c;
+    makespan = std::max(makespan, heap.back());
+    std::push_heap(heap.begin(), heap.end(), cmp);
   }
   return makespan;
 }
@@ -713,19 +747,13 @@ long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_h
 }
 
 int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long long R, bool exact,
-                    long long* ntiles) {
-  const long long key[6] = {L, k_lo, k_hi, R, exact ? -kK : kK, row_hi};
-  if (std::equal(key, key + 6, c->tiles_key)) {
+                    int m, long long* ntiles) {
+  const long long key[7] = {L, k_lo, k_hi, R, exact ? -kK : kK, row_hi, m};
+  if (std::equal(key, key + 7, c->tiles_key)) {
     *ntiles = (long long)c->tiles_h.size();
     return MPROF_OK;
   }
-  c->tiles_h.clear();
-  for (long long kb = k_lo; kb < k_hi; kb += kK) {
-    const long long rend = std::min<long long>(L - kb, row_hi);
-    const long long Rb = block_R(R, std::min<long long>(kK, k_hi - kb), exact);
-    for (long long ra = 0; ra < rend; ra += Rb)
-      c->tiles_h.push_back(make_int4((int)kb, (int)ra, (int)std::min(ra + Rb, rend), 0));
-  }
+  tile_list(L, k_lo, k_hi, row_hi, R, exact, m, c->tiles_h, nullptr);
   const size_t need = c->tiles_h.size() * sizeof(int4);
   void* p = c->tiles_d;
   int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
@@ -733,7 +761,7 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long lo
   if (st != MPROF_OK) return st;
   CK(cudaMemcpyAsync(c->tiles_d, c->tiles_h.data(), need, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // tiles_h may be rebuilt by the next call
-  std::copy(key, key + 6, c->tiles_key);
+  std::copy(key, key + 7, c->tiles_key);
   *ntiles = (long long)c->tiles_h.size();
   return MPROF_OK;
 }
@@ -980,7 +1008,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
       }
     }
   }
-  int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, &out->ntiles);
+  int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, m, &out->ntiles);
   if (st != MPROF_OK) return st;
   SweepParams prm;
   prm.t = d_t;

@@ -221,7 +221,11 @@ struct Znorm : KeyF64 {
   static constexpr bool kCenteredSeed = true;
   static constexpr bool kCovFilter = true;
   static constexpr bool kColScale = COLSCALE;
-  static constexpr int kMinWarps = COLSCALE ? 12 : 16;  // per SM; measured: the +cB ring wants registers
+#ifndef MPROF_ZN_COV_WARPS
+#define MPROF_ZN_COV_WARPS 16
+#endif
+  // per SM; measured: the +cB ring wants registers
+  static constexpr int kMinWarps = COLSCALE ? 12 : MPROF_ZN_COV_WARPS;
   static constexpr int kPairs = kPairsZnorm;
   __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
     return fma(r.x, c.y, fma(c.x, r.y, acc));
