@@ -145,6 +145,11 @@ int32_t mprof_acamp(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_con
  * j; any family. O(L^2 m) on the GPU — the CLI's `--engine oracle` and an exact checker. */
 int32_t mprof_brute_profile(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
                             double* P, int64_t* I);
+/* Brute-force nearest neighbours of selected rows only (same arithmetic as mprof_brute_profile):
+ * row rows[r] into P[r], I[r], r < nrows; a row outside [0, L) is MPROF_E_BAD_ARG. Used for full
+ * exact-argmin checks of sampled rows at sizes where a whole brute-force profile is too slow. */
+int32_t mprof_brute_rows(mprof_ctx* ctx, const double* t, uint64_t n, const mprof_config* cfg,
+                         const int64_t* rows, uint64_t nrows, double* P, int64_t* I);
 
 /* ---- device-resident pipeline ------------------------------------------------------------- */
 /* Sweeps diagonals k in [k_lo, k_hi) ∩ [exclusion, n - m] of series d_t (device, n doubles) and

@@ -260,6 +260,8 @@ EXPORTS = {
     "mprof_ctx_set_progress": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "mprof_brute_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
                                         C.c_void_p, C.c_void_p]),
+    "mprof_brute_rows": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                     C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
 }
 PROGRESS_FN = C.CFUNCTYPE(C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p)
 
@@ -389,6 +391,20 @@ def brute_profile(ts: TimeSeries, cfg: ProfileConfig, ctx: Optional[Context] = N
     _raise(lib().mprof_brute_profile(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
                                      P.ctypes.data, I.ctypes.data))
     return MatrixProfile(P, I, cfg.m, cfg.kind)
+
+
+def brute_rows(ts: TimeSeries, cfg: ProfileConfig, rows, ctx: Optional[Context] = None):
+    """Brute-force (distance, index) of the nearest neighbour of each of `rows` (GPU, the
+    arithmetic of brute_profile). Returns (P, I) arrays of len(rows)."""
+    _check_int_fields(cfg)
+    v = ts.values()
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    P = np.empty(r.size)
+    I = np.empty(r.size, dtype=np.int64)
+    c = _to_c(cfg)
+    _raise(lib().mprof_brute_rows(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
+                                  r.ctypes.data, r.size, P.ctypes.data, I.ctypes.data))
+    return P, I
 
 
 def aamp(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Callable] = None, threads: int = 0,

@@ -314,13 +314,16 @@ __device__ double bf_dist(const double* __restrict__ t, int i, int j, int m, int
 }
 
 // one CTA per row i; lexicographic (distance, j) minimum over admissible j
+// rows == nullptr: every row i < L into P[i], I[i]; else row rows[r] into P[r], I[r], r < nrows.
 __global__ void k_brute(const double* __restrict__ t, int L, int m, int excl, int family, double p,
                         double flat, const double* __restrict__ mean,
                         const double* __restrict__ var, double* __restrict__ P,
-                        int64_t* __restrict__ I) {
+                        int64_t* __restrict__ I, const int64_t* __restrict__ rows, int nrows) {
   __shared__ double sv[32];
   __shared__ int sj[32];
-  for (int i = blockIdx.x; i < L; i += gridDim.x) {
+  const int nout = rows ? nrows : L;
+  for (int r = blockIdx.x; r < nout; r += gridDim.x) {
+    const int i = rows ? (int)rows[r] : r;
     double bv = INFINITY;
     int bj = INT_MAX;
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -338,8 +341,8 @@ __global__ void k_brute(const double* __restrict__ t, int L, int m, int excl, in
     if (threadIdx.x == 0) {
       for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
         if (sv[w] < bv || (sv[w] == bv && sj[w] < bj)) { bv = sv[w]; bj = sj[w]; }
-      P[i] = bj == INT_MAX ? INFINITY : bv;
-      I[i] = bj == INT_MAX ? -1 : bj;
+      P[r] = bj == INT_MAX ? INFINITY : bv;
+      I[r] = bj == INT_MAX ? -1 : bj;
     }
     __syncthreads();
   }
@@ -1647,10 +1650,51 @@ int32_t mprof_brute_profile(mprof_ctx* in, const double* t, uint64_t n, const mp
     k_moments<<<grid_for((long long)L), 256, 0, c->stream>>>(d_t, (int)L, (int)cfg->m, d_mean, d_var);
   k_brute<<<(unsigned)std::min<uint64_t>(L, 148ull * 64), 256, 0, c->stream>>>(
       d_t, (int)L, (int)cfg->m, (int)cfg->exclusion, cfg->family, cfg->p, cfg->flat_threshold,
-      d_mean, d_var, d_P, d_I);
+      d_mean, d_var, d_P, d_I, nullptr, 0);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(P, d_P, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(I, d_I, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return MPROF_OK;
+}
+
+int32_t mprof_brute_rows(mprof_ctx* in, const double* t, uint64_t n, const mprof_config* cfg,
+                         const int64_t* rows, uint64_t nrows, double* P, int64_t* I) {
+  if (!t || !cfg || (nrows && (!rows || !P || !I))) return fail(MPROF_E_BAD_ARG, "null argument");
+  int32_t st = check_series(t, n);
+  if (st != MPROF_OK) return st;
+  st = check_config(n, cfg);
+  if (st != MPROF_OK) return st;
+  const uint64_t L = n - cfg->m + 1;
+  for (uint64_t r = 0; r < nrows; ++r)
+    if (rows[r] < 0 || (uint64_t)rows[r] >= L)
+      return fail(MPROF_E_BAD_ARG, "row %lld outside [0, %llu)", (long long)rows[r], (unsigned long long)L);
+  if (nrows == 0) return MPROF_OK;
+  if (nrows > (uint64_t)INT_MAX) return fail(MPROF_E_TOO_LARGE, "too many rows");
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  const size_t nt = align_up(n * sizeof(double)), nl = align_up(L * sizeof(double)),
+               nr = align_up(nrows * sizeof(double));
+  st = ensure(&c->io, &c->io_bytes, nt + 2 * nl + 3 * nr);
+  if (st != MPROF_OK) return st;
+  char* base = static_cast<char*>(c->io);
+  double* d_t = reinterpret_cast<double*>(base);
+  double* d_mean = reinterpret_cast<double*>(base + nt);
+  double* d_var = reinterpret_cast<double*>(base + nt + nl);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(base + nt + 2 * nl);
+  double* d_P = reinterpret_cast<double*>(base + nt + 2 * nl + nr);
+  int64_t* d_I = reinterpret_cast<int64_t*>(base + nt + 2 * nl + 2 * nr);
+  CK(cudaMemcpyAsync(d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(d_rows, rows, nrows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  if (cfg->family == MPROF_ZNORMALIZED)
+    k_moments<<<grid_for((long long)L), 256, 0, c->stream>>>(d_t, (int)L, (int)cfg->m, d_mean, d_var);
+  k_brute<<<(unsigned)std::min<uint64_t>(nrows, 148ull * 64), 256, 0, c->stream>>>(
+      d_t, (int)L, (int)cfg->m, (int)cfg->exclusion, cfg->family, cfg->p, cfg->flat_threshold,
+      d_mean, d_var, d_P, d_I, d_rows, (int)nrows);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(P, d_P, nrows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(I, d_I, nrows * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return MPROF_OK;
 }

@@ -325,6 +325,22 @@ def test_bands_merge_to_full_profile(mp):
     assert torch.equal(P, P2)
 
 
+def test_brute_rows_match_brute_profile(mp):
+    r = np.random.default_rng(5)
+    t = np.cumsum(r.standard_normal(3000))
+    t[700:760] = t[700]  # flat run (z-norm flat rule)
+    ts = mp.make_time_series(t)
+    rows = np.array([0, 1, 17, 700, 731, 2000, 2936])
+    for kind in (mp.DistanceKind.euclidean(), mp.DistanceKind.pnorm(3.0), mp.DistanceKind.znormalized()):
+        cfg = mp.ProfileConfig(64, kind)
+        cfg.exclusion = 16
+        full = mp.brute_profile(ts, cfg)
+        P, I = mp.brute_rows(ts, cfg, rows)
+        assert np.array_equal(P, full.distances[rows]) and np.array_equal(I, full.nn_index[rows])
+    with pytest.raises(mp.Error):
+        mp.brute_rows(ts, mp.ProfileConfig(64, mp.DistanceKind.euclidean()), [3000])
+
+
 def test_fp64_peak_is_plausible(mp):
     g, ms = mp.fp64_peak()
     assert 5e3 < g < 1e5, g  # GFLOP/s
@@ -347,6 +363,16 @@ def _full_size_checks(mp, t, m, fam, P, I, rows=6, pairs=20000, tol=TOL):
     assert np.all(within(P[rr], best, tol) | (np.abs(P[rr] - best) <= bound)), (P[rr], best)
     dg = oracle.dist_exact(t, rr, I[rr], m, fam)
     assert np.all(within(dg, best, tol) | (np.abs(dg - best) <= bound))
+    # 64 more sampled rows through the GPU brute force (full O(L m) argmin per row, independent
+    # of the sweep): same minimum, and our neighbour is a tie of the brute one
+    rb = r.choice(L, 64, replace=False)
+    kind = kind_of(mp, fam, 2.0)
+    cfg = mp.ProfileConfig(m, kind)
+    Pb, Ib = mp.brute_rows(mp.make_time_series(t), cfg, rb)
+    assert np.all(within(P[rb], Pb, tol) | (np.abs(P[rb] - Pb) <= bound)), (P[rb], Pb)
+    dg = oracle.dist_exact(t, rb, I[rb], m, fam)
+    db = oracle.dist_exact(t, rb, Ib, m, fam)
+    assert np.all(within(dg, db, tol) | (np.abs(dg - db) <= bound))
 
 
 @pytest.mark.slow
