@@ -49,6 +49,30 @@ constexpr int kK = kD * kT;
 // faster; m=256 0.93 -> column-scaled is 1.8x faster)
 constexpr double kZnCovFilterMinSpread = 0.955;
 
+// Experiment / diagnostic switches, read once per process from the environment. The defaults are
+// the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
+struct Knobs {
+  long long rows_per_tile = 0;  // MPROF_ROWS_PER_TILE: fixed rows per tile (0 = choose_R)
+  bool tile_debug = false;      // MPROF_TILE_DEBUG: print the schedule model's candidates
+  bool tile_order_lpt = false;  // MPROF_TILE_ORDER_LPT: longest-first tile order
+  int zn_filter = 0;            // MPROF_ZN_FILTER=cov|col: force the z-norm filter form
+  bool zn_no_near = false;      // MPROF_ZN_NO_NEAR: no column-scaled near-diagonal block
+  bool stats = false;           // MPROF_STATS: count replays / offers (stderr)
+};
+const Knobs& knobs() {
+  static const Knobs k = [] {
+    Knobs r;
+    if (const char* e = getenv("MPROF_ROWS_PER_TILE")) r.rows_per_tile = std::max(1LL, atoll(e));
+    r.tile_debug = getenv("MPROF_TILE_DEBUG") != nullptr;
+    r.tile_order_lpt = getenv("MPROF_TILE_ORDER_LPT") != nullptr;
+    if (const char* e = getenv("MPROF_ZN_FILTER")) r.zn_filter = !strcmp(e, "cov") ? 1 : !strcmp(e, "col") ? 2 : 0;
+    r.zn_no_near = getenv("MPROF_ZN_NO_NEAR") != nullptr;
+    r.stats = getenv("MPROF_STATS") != nullptr;
+    return r;
+  }();
+  return k;
+}
+
 thread_local std::string g_last_error;
 
 int32_t fail(int32_t code, const char* fmt, ...) {
@@ -676,7 +700,7 @@ void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, i
     }
     if (kb == k_lo) first_block = tiles.size();
   }
-  if (getenv("MPROF_TILE_ORDER_LPT")) {  // experiments: decreasing cost after the first block
+  if (knobs().tile_order_lpt) {  // experiments: decreasing cost after the first block
     std::vector<size_t> ord(tiles.size());
     for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
     std::stable_sort(ord.begin() + first_block, ord.end(),
@@ -726,7 +750,7 @@ long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_h
   Rmax = (Rmax + kS - 1) / kS * kS;
   if (cfg->refresh_interval > 0) Rmax = std::min<long long>(Rmax, (long long)cfg->refresh_interval);
   long long R = Rmax;
-  if (const char* e = getenv("MPROF_ROWS_PER_TILE")) return std::max(1LL, atoll(e));  // experiments
+  if (knobs().rows_per_tile) return knobs().rows_per_tile;  // experiments
   if (Rmax > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, Rmax) < 16LL * slots) {
     double best = schedule_makespan(L, k_lo, k_hi, row_hi, Rmax, slots, (int)cfg->m);
     long long prev = Rmax;
@@ -736,7 +760,7 @@ long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_h
       prev = Rj;
       if (count_tiles(L, k_lo, k_hi, row_hi, Rj) > 32LL * slots) break;
       const double ms = schedule_makespan(L, k_lo, k_hi, row_hi, Rj, slots, (int)cfg->m);
-      if (getenv("MPROF_TILE_DEBUG"))
+      if (knobs().tile_debug)
         fprintf(stderr, "[mprof tiles] slots %d R %lld tiles %lld makespan %.0f (R_max %.0f)\n", slots,
                 Rj, count_tiles(L, k_lo, k_hi, row_hi, Rj), ms, best);
       if (ms < best * (1.0 - 1e-3)) {
@@ -933,11 +957,10 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     if (st != MPROF_OK) return st;
     k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
     *launches += 2;
-    // filter form for this series: MPROF_ZN_FILTER=cov|col overrides the measured choice
-    const char* force = getenv("MPROF_ZN_FILTER");
-    if (force && !strcmp(force, "cov")) {
+    // filter form for this series (MPROF_ZN_FILTER=cov|col overrides the measured choice)
+    if (knobs().zn_filter == 1) {
       c->zn_colscale = false;
-    } else if (force && !strcmp(force, "col")) {
+    } else if (knobs().zn_filter == 2) {
       c->zn_colscale = true;
     } else {
       if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
@@ -1005,7 +1028,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
       out->R = c->R_val;
     } else {
       out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg));
-      if (!getenv("MPROF_ROWS_PER_TILE")) {
+      if (!knobs().rows_per_tile) {
         std::copy(key, key + 9, c->R_key);
         c->R_val = out->R;
       }
@@ -1031,14 +1054,14 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   prm.rl = rl;
   prm.p = cfg->p;
   prm.stats = nullptr;
-  const bool want_stats = getenv("MPROF_STATS") != nullptr;
+  const bool want_stats = knobs().stats;
   if (want_stats) {
     CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
   }
   long long n_near = 0;
   if (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale && !cfg->exact &&
-      k_tile <= (int)cfg->exclusion + 1 && !getenv("MPROF_ZN_NO_NEAR"))
+      k_tile <= (int)cfg->exclusion + 1 && !knobs().zn_no_near)
     n_near = count_tiles(L, k_tile, std::min(k_tile + kK, k_hi), row_hi, out->R);  // first block
   st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
                       &out->ms);

@@ -1,8 +1,15 @@
 """Sweep time of arbitrary C4 diagonal ranges under several rows-per-tile settings (experiments).
-usage: time_ranges.py FAMILY R1,R2,.. lo:hi [lo:hi ...]   (R=0 -> library's choice)"""
+usage: time_ranges.py FAMILY R1,R2,.. lo:hi [lo:hi ...]   (R=0 -> library's choice)
+The library reads MPROF_ROWS_PER_TILE once per process, so each R runs in its own process."""
 import os
+import subprocess
 import sys
 from pathlib import Path
+
+if len(sys.argv[2].split(",")) > 1:
+    for R in sys.argv[2].split(","):
+        subprocess.run([sys.executable, __file__, sys.argv[1], R, *sys.argv[3:]], check=True)
+    sys.exit(0)
 
 import torch
 
