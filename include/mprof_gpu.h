@@ -202,6 +202,20 @@ int32_t mprof_state_profile(mprof_state* st, double* P, int64_t* I, double* cmp)
 int32_t mprof_state_series(const mprof_state* st, double* t);
 void mprof_state_destroy(mprof_state* st);
 
+/* ---- one process, several GPUs ------------------------------------------------------------ */
+/* The entry points above on `ndev` devices: the admissible diagonals are split into equal-area
+ * bands (mprof_band_cuts), device devices[g] sweeps band g from its own host thread and context,
+ * the partial profiles are merged on devices[0] (peer copies over NVLink + the lexicographic
+ * merge kernel, = MinBuffer::absorb, /root/reference/proj/src/detail/diag_scan.hpp:45-52) and
+ * finalized there. engine: 0 = mprof_aamp, 1 = mprof_aamp_pnorm, 2 = mprof_acamp (same
+ * validation and BadKind rule; both AcampVariants give the same profile). A device may be listed
+ * more than once. This replaces the reference's `threads` worker split
+ * (/root/reference/proj/src/detail/diag_scan.hpp:228-256) with a device split; progress
+ * observers are not called. */
+int32_t mprof_profile_multi(const int32_t* devices, uint32_t ndev, int32_t engine, const double* t,
+                            uint64_t n, const mprof_config* cfg, double* P, int64_t* I,
+                            mprof_run_info* info);
+
 /* ---- multi-GPU partition (host-side math, no device needed) ------------------------------ */
 /* Equal-area cut of the diagonal range [exclusion, n-m] into `parts` contiguous bands; writes
  * parts+1 boundaries (cuts[0] = exclusion, cuts[parts] = n-m+1). Area(k) = L - k cells. Interior

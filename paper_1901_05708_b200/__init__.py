@@ -262,6 +262,8 @@ EXPORTS = {
                                         C.c_void_p, C.c_void_p]),
     "mprof_brute_rows": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
                                      C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "mprof_profile_multi": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_int32, C.c_void_p, C.c_uint64,
+                                        C.POINTER(_Config), C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 PROGRESS_FN = C.CFUNCTYPE(C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p)
 
@@ -391,6 +393,26 @@ def brute_profile(ts: TimeSeries, cfg: ProfileConfig, ctx: Optional[Context] = N
     _raise(lib().mprof_brute_profile(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
                                      P.ctypes.data, I.ctypes.data))
     return MatrixProfile(P, I, cfg.m, cfg.kind)
+
+
+ENGINES = {"aamp": 0, "aamp_pnorm": 1, "acamp": 2}
+
+
+def profile_multi(ts: TimeSeries, cfg: ProfileConfig, devices, engine: str = "aamp") -> MatrixProfile:
+    """One process, several GPUs (mprof_profile_multi): equal-area diagonal bands, one per entry
+    of `devices` (a device may repeat), merged on devices[0]. engine: aamp | aamp_pnorm | acamp."""
+    _check_int_fields(cfg)
+    v = ts.values()
+    n = v.shape[0]
+    L = max(n - cfg.m + 1, 0)
+    P = np.empty(L, dtype=np.float64)
+    I = np.empty(L, dtype=np.int64)
+    info = RunInfo()
+    d = np.ascontiguousarray(devices, dtype=np.int32)
+    c = _to_c(cfg)
+    _raise(lib().mprof_profile_multi(d.ctypes.data, d.size, ENGINES[engine], v.ctypes.data, n,
+                                     C.byref(c), P.ctypes.data, I.ctypes.data, C.byref(info)))
+    return MatrixProfile(P, I, cfg.m, cfg.kind, info)
 
 
 def brute_rows(ts: TimeSeries, cfg: ProfileConfig, rows, ctx: Optional[Context] = None):

@@ -18,6 +18,7 @@
 #include "mprof/acamp.hpp"
 #include "mprof/bench.hpp"
 #include "mprof/csv_io.hpp"
+#include "mprof/multi_gpu.hpp"
 #include "mprof/oracle.hpp"
 
 namespace {
@@ -134,6 +135,7 @@ int compute(int argc, char** argv) {
   c.add("engine", "auto = the diagonal sweep on the GPU; oracle = brute force (GPU)").choices = {"auto", "oracle"};
   c.add("acamp-variant", "znorm comparison space: f | sq").choices = {"f", "sq"};
   c.add("threads", "accepted for compatibility (the GPU sweep ignores it)");
+  c.add("devices", "comma-separated CUDA devices to split the diagonals across (default: one)");
   c.add("progress", "emit percent lines to standard error", true);
   if (!c.parse(argc, argv, 2)) return 0;
 
@@ -176,9 +178,18 @@ int compute(int argc, char** argv) {
     };
   }
   const bool oracle = c.seen("engine") && c.str("engine") == "oracle";
+  std::vector<int> devices;
+  if (c.seen("devices"))
+    for (const auto& d : split(c.str("devices"))) devices.push_back(static_cast<int>(to_size("devices", d)));
+  if (c.seen("devices") && devices.empty()) throw UsageError("--devices: expected a device list");
   mprof::MatrixProfile profile;
   if (oracle) {
     profile = mprof::brute_profile(ts, cfg);
+  } else if (!devices.empty()) {
+    const auto engine = kind.family == mprof::DistanceFamily::PNorm        ? mprof::Engine::AampPnorm
+                        : kind.family == mprof::DistanceFamily::ZNormalized ? mprof::Engine::Acamp
+                                                                            : mprof::Engine::Aamp;
+    profile = mprof::profile_on_devices(ts, cfg, devices, engine);
   } else if (kind.family == mprof::DistanceFamily::PNorm) {
     profile = mprof::aamp_pnorm(ts, cfg, progress);
   } else if (kind.family == mprof::DistanceFamily::ZNormalized) {

@@ -17,6 +17,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -401,6 +402,14 @@ __global__ void k_init_from_prev(BestEntry* __restrict__ best, const double* __r
 __global__ void k_unreverse(const BestEntry* __restrict__ in, BestEntry* __restrict__ out, int L) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
     out[i] = in[L - 1 - i];
+}
+
+// An empty partial profile (a band without diagonals): +inf / no neighbour.
+__global__ void k_split_empty(double* __restrict__ cmp, int64_t* __restrict__ idx, int L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    cmp[i] = INFINITY;
+    idx[i] = -1;
+  }
 }
 
 __global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__ cmp,
@@ -1427,6 +1436,151 @@ int32_t mprof_merge_device(mprof_ctx* in, double* d_cmp, int64_t* d_idx, const d
   k_merge<<<grid_for((long long)L), 256, 0, c->stream>>>(d_cmp, d_idx, d_ocmp, d_oidx, (int)L);
   CK(cudaGetLastError());
   return MPROF_OK;
+}
+
+int32_t mprof_profile_multi(const int32_t* devices, uint32_t ndev, int32_t engine, const double* t,
+                            uint64_t n, const mprof_config* cfg, double* P, int64_t* I,
+                            mprof_run_info* info) {
+  if (!devices || ndev == 0 || !t || !cfg || !P || !I) return fail(MPROF_E_BAD_ARG, "null argument");
+  if (engine < 0 || engine > 2) return fail(MPROF_E_BAD_ARG, "unknown engine %d", engine);
+  int32_t st = check_series(t, n);
+  if (st != MPROF_OK) return st;
+  st = check_config(n, cfg);
+  if (st != MPROF_OK) return st;
+  static const int32_t fam[] = {MPROF_EUCLIDEAN, MPROF_PNORM, MPROF_ZNORMALIZED};
+  static const char* msg[] = {"aamp computes Euclidean profiles only",
+                              "aamp_pnorm requires a p-norm distance kind",
+                              "acamp requires the z-normalized distance kind"};
+  if (cfg->family != fam[engine]) return fail(MPROF_E_BAD_KIND, "%s", msg[engine]);
+  int count = 0, caller_dev = 0;
+  CK(cudaGetDeviceCount(&count));
+  CK(cudaGetDevice(&caller_dev));
+  for (uint32_t g = 0; g < ndev; ++g)
+    if (devices[g] < 0 || devices[g] >= count)
+      return fail(MPROF_E_CUDA, "no CUDA device %d (%d present)", devices[g], count);
+  const uint64_t L = n - cfg->m + 1;
+  std::vector<uint64_t> cuts(ndev + 1);
+  st = mprof_band_cuts(n, cfg->m, cfg->exclusion, ndev, cuts.data());
+  if (st != MPROF_OK) return st;
+
+  // one context, stream and buffer set per band (a device listed twice gets two contexts)
+  struct Part {
+    int dev = 0;
+    mprof_ctx* ctx = nullptr;
+    double* d_t = nullptr;
+    double* d_cmp = nullptr;
+    int64_t* d_idx = nullptr;
+    mprof_run_info info{};
+    int32_t st = MPROF_OK;
+    std::string err;
+  };
+  std::vector<Part> parts(ndev);
+  auto release = [&]() {
+    for (auto& q : parts) {
+      if (!q.ctx) continue;
+      cudaSetDevice(q.dev);
+      cudaStreamSynchronize(q.ctx->stream);
+      cudaFree(q.d_t);
+      cudaFree(q.d_cmp);
+      cudaFree(q.d_idx);
+      mprof_ctx_destroy(q.ctx);
+      q.ctx = nullptr;
+    }
+  };
+  auto work = [&](uint32_t g) {
+    Part& q = parts[g];
+    q.dev = devices[g];
+    q.st = [&]() -> int32_t {
+      int32_t s = mprof_ctx_create(q.dev, &q.ctx);
+      if (s != MPROF_OK) return s;
+      CK(cudaMalloc(&q.d_t, n * sizeof(double)));
+      CK(cudaMalloc(&q.d_cmp, L * sizeof(double)));
+      CK(cudaMalloc(&q.d_idx, L * sizeof(int64_t)));
+      CK(cudaMemcpyAsync(q.d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, q.ctx->stream));
+      if (cuts[g] >= cuts[g + 1]) {  // empty band: an all-empty partial profile
+        k_split_empty<<<grid_for((long long)L), 256, 0, q.ctx->stream>>>(q.d_cmp, q.d_idx, (int)L);
+        CK(cudaGetLastError());
+      } else {
+        s = sweep_impl(q.ctx, q.d_t, n, cfg, cuts[g], cuts[g + 1], q.d_cmp, q.d_idx, &q.info);
+        if (s != MPROF_OK) return s;
+      }
+      CK(cudaStreamSynchronize(q.ctx->stream));
+      return MPROF_OK;
+    }();
+    if (q.st != MPROF_OK) q.err = g_last_error;
+  };
+  {
+    std::vector<std::thread> pool;
+    for (uint32_t g = 1; g < ndev; ++g) pool.emplace_back(work, g);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  for (auto& q : parts)
+    if (q.st != MPROF_OK) {
+      const int32_t s = q.st;
+      const std::string e = q.err;
+      release();
+      g_last_error = e;
+      cudaSetDevice(caller_dev);
+      return s;
+    }
+  // merge the partial profiles on the first device (peer copies over NVLink, then the
+  // lexicographic MinBuffer::absorb kernel), finalize there
+  Part& p0 = parts[0];
+  mprof_ctx* c0 = p0.ctx;
+  auto finish = [&]() -> int32_t {
+    CK(cudaSetDevice(p0.dev));
+    double* s_cmp = nullptr;
+    int64_t* s_idx = nullptr;
+    double* d_P = nullptr;
+    CK(cudaMalloc(&d_P, L * sizeof(double)));
+    if (ndev > 1) {
+      CK(cudaMalloc(&s_cmp, L * sizeof(double)));
+      CK(cudaMalloc(&s_idx, L * sizeof(int64_t)));
+    }
+    int32_t s = MPROF_OK;
+    for (uint32_t g = 1; g < ndev && s == MPROF_OK; ++g) {
+      const Part& q = parts[g];
+      if (q.dev != p0.dev) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(q.dev, 0);
+        if (e != cudaSuccess) cudaGetLastError();  // already enabled / no P2P: copies still work
+      }
+      CK(cudaMemcpyPeerAsync(s_cmp, p0.dev, q.d_cmp, q.dev, L * sizeof(double), c0->stream));
+      CK(cudaMemcpyPeerAsync(s_idx, p0.dev, q.d_idx, q.dev, L * sizeof(int64_t), c0->stream));
+      s = mprof_merge_device(c0, p0.d_cmp, p0.d_idx, s_cmp, s_idx, L);
+    }
+    if (s == MPROF_OK) s = mprof_finalize_device(c0, p0.d_t, n, p0.d_cmp, p0.d_idx, cfg, d_P);
+    if (s == MPROF_OK) {
+      CK(cudaMemcpyAsync(P, d_P, L * sizeof(double), cudaMemcpyDeviceToHost, c0->stream));
+      CK(cudaMemcpyAsync(I, p0.d_idx, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c0->stream));
+      CK(cudaStreamSynchronize(c0->stream));
+    }
+    cudaFree(d_P);
+    cudaFree(s_cmp);
+    cudaFree(s_idx);
+    return s;
+  };
+  st = finish();
+  if (st == MPROF_OK && info) {
+    *info = parts[0].info;
+    info->cells = 0;
+    info->tiles = 0;
+    info->kernel_launches = 0;
+    info->sweep_ms = 0.f;
+    for (const auto& q : parts) {
+      info->cells += q.info.cells;
+      info->tiles += q.info.tiles;
+      info->kernel_launches += q.info.kernel_launches;
+      info->sweep_ms = std::max(info->sweep_ms, q.info.sweep_ms);
+    }
+    info->diagonals = L - cfg->exclusion;
+    info->kernel_launches += 2 * (ndev - 1) + 1;  // merges (+copies) and the finalize
+  }
+  const std::string keep = g_last_error;
+  release();
+  g_last_error = keep;
+  cudaSetDevice(caller_dev);
+  return st;
 }
 
 uint64_t mprof_band_cells(uint64_t n, uint64_t m, uint64_t k_lo, uint64_t k_hi) {

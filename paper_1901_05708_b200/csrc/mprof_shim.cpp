@@ -9,6 +9,7 @@
 #include "mprof/acamp.hpp"
 #include "mprof/core.hpp"
 #include "mprof/engine_state.hpp"
+#include "mprof/multi_gpu.hpp"
 #include "mprof/oracle.hpp"
 #include "mprof_gpu.h"
 
@@ -115,6 +116,15 @@ MatrixProfile acamp(const TimeSeries& ts, const ProfileConfig& cfg, AcampVariant
 MatrixProfile brute_profile(const TimeSeries& ts, const ProfileConfig& cfg) {
   return run(ts, cfg, {}, [&](const mprof_config* c, double* P, int64_t* I, mprof_run_info*) {
     return mprof_brute_profile(nullptr, ts.data(), ts.size(), c, P, I);
+  });
+}
+
+MatrixProfile profile_on_devices(const TimeSeries& ts, const ProfileConfig& cfg,
+                                 std::span<const int> devices, Engine engine) {
+  std::vector<int32_t> dev(devices.begin(), devices.end());
+  return run(ts, cfg, {}, [&](const mprof_config* c, double* P, int64_t* I, mprof_run_info* info) {
+    return mprof_profile_multi(dev.data(), static_cast<uint32_t>(dev.size()),
+                               static_cast<int32_t>(engine), ts.data(), ts.size(), c, P, I, info);
   });
 }
 

@@ -91,6 +91,14 @@ def test_cli_engines_agree(mp, tmp_path):
     fa, _ = parse_profile(sh(base + " --acamp-variant f").stdout)
     fs, _ = parse_profile(sh(base + " --acamp-variant sq").stdout)
     assert np.all(np.abs(fa - fs) <= 1e-9 * np.maximum(1, np.abs(fs)))
+    # diagonals split across devices (here two bands on device 0) give the same profile
+    for d in ("znorm", "euclidean", "pnorm --p 3"):
+        one = f"{CLI} compute --input {f2} --m 11 --distance {d}"
+        x, ix = parse_profile(sh(one).stdout)
+        y, iy = parse_profile(sh(one + " --devices 0,0").stdout)
+        assert np.all(np.abs(x - y) <= 1e-8 * np.maximum(1, np.abs(x)))  # I may differ on ties only
+    bad = sh(base + " --devices 0,,x")
+    assert bad.returncode == 2
 
 
 @pytest.mark.gpu

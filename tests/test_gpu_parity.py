@@ -325,6 +325,37 @@ def test_bands_merge_to_full_profile(mp):
     assert torch.equal(P, P2)
 
 
+def test_profile_multi_equals_single(mp):
+    """One process, several devices: bands on separate contexts (here all on device 0, run
+    concurrently without waiting on each other), peer-copy merge, finalize on the first device."""
+    r = np.random.default_rng(33)
+    t = 10 + np.cumsum(r.standard_normal(8000))
+    t[5000:5400] = t[5000]  # flat run (z-norm)
+    ts = mp.make_time_series(t)
+    m = 128
+    for engine, fam, p in (("aamp", EUCLIDEAN, 2.0), ("aamp_pnorm", PNORM, 3.0), ("acamp", ZNORM, 2.0)):
+        cfg = mp.ProfileConfig(m, kind_of(mp, fam, p))
+        _, Pr, Ir = oracle.scan(t, m, fam, p)
+        for devices in ([0], [0, 0], [0, 0, 0]):
+            multi = mp.profile_multi(ts, cfg, devices, engine)
+            assert_parity(t, m, fam, p, multi.distances, multi.nn_index, Pr, Ir)
+        if fam != ZNORM:  # parity build: bands + merge are bit-identical to one device
+            cfg.exact, cfg.refresh_interval = True, 512
+            single = getattr(mp, engine)(ts, cfg)
+            multi = mp.profile_multi(ts, cfg, [0, 0, 0], engine)
+            assert np.array_equal(multi.nn_index, single.nn_index)
+            assert np.array_equal(multi.distances, single.distances)
+    # validation and the BadKind rule of the single-device entry points
+    with pytest.raises(mp.Error) as e:
+        mp.profile_multi(ts, mp.ProfileConfig(128, mp.DistanceKind.euclidean()), [0], "acamp")
+    assert e.value.code == mp.ErrorCode.BadKind
+    # more bands than diagonals: empty bands contribute nothing
+    small = mp.make_time_series(t[:40])
+    cfg = mp.ProfileConfig(30, mp.DistanceKind.euclidean())
+    a, b = mp.aamp(small, cfg), mp.profile_multi(small, cfg, [0] * 16)
+    assert np.array_equal(a.nn_index, b.nn_index) and np.all(within(a.distances, b.distances, 1e-12))
+
+
 def test_brute_rows_match_brute_profile(mp):
     r = np.random.default_rng(5)
     t = np.cumsum(r.standard_normal(3000))
