@@ -535,7 +535,7 @@ struct mprof_ctx {
   std::vector<int4> tiles_h;  // (first diagonal, first row, row end, -)
   int4* tiles_d = nullptr;
   size_t tiles_cap = 0;
-  long long tiles_key[7] = {-1, -1, -1, -1, -1, -1, -1};
+  long long tiles_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   long long R_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // rows-per-tile choice cache
   long long R_val = 0;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
@@ -659,15 +659,16 @@ int32_t ensure_znorm_stats(mprof_ctx* c, const double* d_t, uint64_t n, const mp
 // Rows per tile of a diagonal block w < K diagonals wide (a band's last block): a narrow tile is
 // latency-bound per row (a thin tile of R rows costs ~3/4 of a full one), so its rows shrink with
 // its width. Exact mode keeps R: runs are seeded at multiples of refresh_interval.
-long long block_R(long long R, long long w, bool exact) {
+// S = the sweep policy's rows per shared-memory stage (stage_rows_for).
+long long block_R(long long R, long long w, bool exact, int S) {
   if (exact || w >= kK) return R;
-  return std::min(R, std::max<long long>(2 * kS, (R * w / kK + kS - 1) / kS * kS));
+  return std::min(R, std::max<long long>(2 * S, (R * w / kK + S - 1) / S * S));
 }
 
-long long count_tiles(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact = false) {
+long long count_tiles(int L, int k_lo, int k_hi, int row_hi, long long R, int S, bool exact = false) {
   long long t = 0;
   for (long long kb = k_lo; kb < k_hi; kb += kK) {
-    const long long Rb = block_R(R, std::min<long long>(kK, k_hi - kb), exact);
+    const long long Rb = block_R(R, std::min<long long>(kK, k_hi - kb), exact, S);
     t += (std::min<long long>(L - kb, row_hi) + Rb - 1) / Rb;
   }
   return t;
@@ -692,16 +693,16 @@ double tile_cells(long long L, long long kb, long long k_hi, long long row_hi, l
 // diagonal-block order; the first block's tiles come first (they may run on the near-diagonal
 // side stream, dispatch_sweep). Longest-first ordering of the partial tiles was measured: +1 %
 // on C4 AAMP, -11 % on C3 (MPROF_TILE_ORDER_LPT keeps it available for experiments).
-void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, int m,
+void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, int m, int S,
                std::vector<int4>& tiles, std::vector<double>* costs) {
   tiles.clear();
   std::vector<double> cost;
-  const double fixed = (double)m / 3.0 + 2.0 * kS;
+  const double fixed = (double)m / 3.0 + 2.0 * S;
   size_t first_block = 0;
   for (long long kb = k_lo; kb < k_hi; kb += kK) {
     const long long w = std::min<long long>(kK, k_hi - kb);
     const long long rend = std::min<long long>(L - kb, row_hi);
-    const long long Rb = block_R(R, w, exact);
+    const long long Rb = block_R(R, w, exact, S);
     for (long long ra = 0; ra < rend; ra += Rb) {
       tiles.push_back(make_int4((int)kb, (int)ra, (int)std::min(ra + Rb, rend), 0));
       const double cells = tile_cells(L, kb, k_hi, row_hi, ra, Rb);
@@ -729,10 +730,11 @@ void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, i
 // Makespan (in row-steps of a full-width tile) of the tile list in launch order on `slots`
 // resident CTAs: the block scheduler hands the next tile to the first free slot (list
 // scheduling).
-double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int slots, int m) {
+double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int slots, int m,
+                         int S) {
   std::vector<int4> tiles;
   std::vector<double> cost;
-  tile_list(L, k_lo, k_hi, row_hi, R, false, m, tiles, &cost);
+  tile_list(L, k_lo, k_hi, row_hi, R, false, m, S, tiles, &cost);
   std::vector<double> heap(slots, 0.0);  // min-heap of slot free times
   auto cmp = std::greater<double>();
   double makespan = 0.0;
@@ -750,46 +752,47 @@ double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int
 // scheduled on the sweep kernel's real residency (slots = occupancy x SMs) and the shortest
 // makespan wins (ties -> longer tiles). Grids of >= 16 waves keep R_max (tail < ~3 %). The
 // choice is cached per context and shape (the simulation costs up to a few ms of host time).
-long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int slots) {
+long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int slots,
+                   int S) {
   if (cfg->exact) {
     if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
     return L;  // the whole diagonal is one run, like the reference's refresh = 0
   }
-  long long Rmax = std::max<long long>(32LL * (long long)cfg->m, 8LL * kS);
-  Rmax = (Rmax + kS - 1) / kS * kS;
+  long long Rmax = std::max<long long>(32LL * (long long)cfg->m, 8LL * S);
+  Rmax = (Rmax + S - 1) / S * S;
   if (cfg->refresh_interval > 0) Rmax = std::min<long long>(Rmax, (long long)cfg->refresh_interval);
   long long R = Rmax;
   if (knobs().rows_per_tile) return knobs().rows_per_tile;  // experiments
-  if (Rmax > 2 * kS && count_tiles(L, k_lo, k_hi, row_hi, Rmax) < 16LL * slots) {
-    double best = schedule_makespan(L, k_lo, k_hi, row_hi, Rmax, slots, (int)cfg->m);
+  if (Rmax > 2 * S && count_tiles(L, k_lo, k_hi, row_hi, Rmax, S) < 16LL * slots) {
+    double best = schedule_makespan(L, k_lo, k_hi, row_hi, Rmax, slots, (int)cfg->m, S);
     long long prev = Rmax;
     for (int j = 2; j <= 32; ++j) {
-      const long long Rj = std::max<long long>(2 * kS, (Rmax / j + kS - 1) / kS * kS);
+      const long long Rj = std::max<long long>(2 * S, (Rmax / j + S - 1) / S * S);
       if (Rj >= prev) continue;
       prev = Rj;
-      if (count_tiles(L, k_lo, k_hi, row_hi, Rj) > 32LL * slots) break;
-      const double ms = schedule_makespan(L, k_lo, k_hi, row_hi, Rj, slots, (int)cfg->m);
+      if (count_tiles(L, k_lo, k_hi, row_hi, Rj, S) > 32LL * slots) break;
+      const double ms = schedule_makespan(L, k_lo, k_hi, row_hi, Rj, slots, (int)cfg->m, S);
       if (knobs().tile_debug)
         fprintf(stderr, "[mprof tiles] slots %d R %lld tiles %lld makespan %.0f (R_max %.0f)\n", slots,
-                Rj, count_tiles(L, k_lo, k_hi, row_hi, Rj), ms, best);
+                Rj, count_tiles(L, k_lo, k_hi, row_hi, Rj, S), ms, best);
       if (ms < best * (1.0 - 1e-3)) {
         best = ms;
         R = Rj;
       }
-      if (Rj == 2 * kS) break;
+      if (Rj == 2 * S) break;
     }
   }
   return R;
 }
 
 int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long long R, bool exact,
-                    int m, long long* ntiles) {
-  const long long key[7] = {L, k_lo, k_hi, R, exact ? -kK : kK, row_hi, m};
-  if (std::equal(key, key + 7, c->tiles_key)) {
+                    int m, int S, long long* ntiles) {
+  const long long key[8] = {L, k_lo, k_hi, R, exact ? -kK : kK, row_hi, m, S};
+  if (std::equal(key, key + 8, c->tiles_key)) {
     *ntiles = (long long)c->tiles_h.size();
     return MPROF_OK;
   }
-  tile_list(L, k_lo, k_hi, row_hi, R, exact, m, c->tiles_h, nullptr);
+  tile_list(L, k_lo, k_hi, row_hi, R, exact, m, S, c->tiles_h, nullptr);
   const size_t need = c->tiles_h.size() * sizeof(int4);
   void* p = c->tiles_d;
   int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
@@ -797,7 +800,7 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long lo
   if (st != MPROF_OK) return st;
   CK(cudaMemcpyAsync(c->tiles_d, c->tiles_h.data(), need, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // tiles_h may be rebuilt by the next call
-  std::copy(key, key + 7, c->tiles_key);
+  std::copy(key, key + 8, c->tiles_key);
   *ntiles = (long long)c->tiles_h.size();
   return MPROF_OK;
 }
@@ -819,13 +822,23 @@ int32_t launch_first_diag(mprof_ctx* c, const SweepParams& prm, int k1, uint32_t
   return MPROF_OK;
 }
 
+// Rows per shared-memory stage of the policy's kernel: the policy's own choice if it has one,
+// else the build's (longer stages halve the per-stage barrier/threshold-refresh overhead; only
+// the policies where that measured faster ask for them).
+template <class P>
+constexpr int stage_rows() {
+  if constexpr (requires { P::kStageRows; }) return P::kStageRows;
+  else return kS;
+}
+
 // Tiles [t0, t0 + nt) of the tile table on stream s.
 template <class P>
 int32_t launch_tiles(SweepParams prm, long long t0, long long nt, cudaStream_t s, uint32_t* launches) {
   if (nt <= 0) return MPROF_OK;
-  using SM = SweepSmem<P, kD, kT, kS>;
+  constexpr int S = stage_rows<P>();
+  using SM = SweepSmem<P, kD, kT, S>;
   const size_t smem = sizeof(SM);
-  auto kern = sweep_kernel<P, kD, kT, kS, min_blocks<P>()>;
+  auto kern = sweep_kernel<P, kD, kT, S, min_blocks<P>()>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prm.tiles += t0;
   kern<<<(unsigned)nt, kT, smem, s>>>(prm);
@@ -913,8 +926,8 @@ int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams&
 int sweep_blocks_per_sm(const mprof_ctx* c, const mprof_config* cfg) {
   int nb = 1;
   with_policy(c, cfg, [&]<class P>() {
-    using SM = SweepSmem<P, kD, kT, kS>;
-    auto kern = sweep_kernel<P, kD, kT, kS, min_blocks<P>()>;
+    using SM = SweepSmem<P, kD, kT, stage_rows<P>()>;
+    auto kern = sweep_kernel<P, kD, kT, stage_rows<P>(), min_blocks<P>()>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SM)) ==
             cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kT, sizeof(SM)) != cudaSuccess)
@@ -923,6 +936,10 @@ int sweep_blocks_per_sm(const mprof_ctx* c, const mprof_config* cfg) {
     return 0;
   });
   return std::max(1, nb);
+}
+
+int stage_rows_for(const mprof_ctx* c, const mprof_config* cfg) {
+  return with_policy(c, cfg, [&]<class P>() { return stage_rows<P>(); });
 }
 
 int32_t check_config(uint64_t n, const mprof_config* cfg) {
@@ -1026,6 +1043,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   // would re-offer values equal to the thresholds they set (every block of those lanes replays
   // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
   const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
+  const int S = stage_rows_for(c, cfg);
   {
     long long pbits;
     std::memcpy(&pbits, &cfg->p, sizeof pbits);
@@ -1036,14 +1054,14 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     if (std::equal(key, key + 9, c->R_key)) {
       out->R = c->R_val;
     } else {
-      out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg));
+      out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg), S);
       if (!knobs().rows_per_tile) {
         std::copy(key, key + 9, c->R_key);
         c->R_val = out->R;
       }
     }
   }
-  int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, m, &out->ntiles);
+  int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, m, S, &out->ntiles);
   if (st != MPROF_OK) return st;
   SweepParams prm;
   prm.t = d_t;
@@ -1071,7 +1089,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   long long n_near = 0;
   if (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale && !cfg->exact &&
       k_tile <= (int)cfg->exclusion + 1 && !knobs().zn_no_near)
-    n_near = count_tiles(L, k_tile, std::min(k_tile + kK, k_hi), row_hi, out->R);  // first block
+    n_near = count_tiles(L, k_tile, std::min(k_tile + kK, k_hi), row_hi, out->R, S);  // first block
   st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
                       &out->ms);
   if (st != MPROF_OK) return st;

@@ -113,6 +113,12 @@ struct Euclid : KeyF64 {
   using V = double;
   using V2 = double2;
   using VB = double;
+  #ifndef MPROF_STAGE_WIDE
+#define MPROF_STAGE_WIDE 256
+#endif
+  // 256-row stages: C4 -1.2 % (AAMP keeps 4 CTAs/SM). Tried for the covariance-only z-norm
+  // kernel too: C4 -1.2 % but C5 +2 % (its larger shared memory drops it to 3 CTAs/SM).
+  static constexpr int kStageRows = EXACT ? 128 : MPROF_STAGE_WIDE;
   static constexpr bool kHasB = false;
   static constexpr bool kCenteredSeed = false;
   static constexpr bool kCovFilter = false;
