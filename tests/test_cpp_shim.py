@@ -1,5 +1,7 @@
 """The C++ drop-in (include/mprof/*.hpp): reference-style code compiles and links against
-libmprof_gpu.so; on a GPU it reproduces the reference's known answers."""
+libmprof_gpu.so; on a GPU it reproduces the reference's known answers and exercises ProgressFn
+(ticks + cancellation), build_engine_state / extend_profile, brute_profile and the multi-device
+entry point (tests/cpp/shim_demo.cpp)."""
 import subprocess
 from pathlib import Path
 
