@@ -678,52 +678,60 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
   using G = Geo<D, T, S>;
   using SM = SweepSmem<P, D, T, S>;
   using VB = typename P::VB;
-  // the columns one thread's block touches are [cD, cD + 2D - 1): two aligned blocks, read from
-  // the raw words (no dependency on other threads' results of this call)
-  for (int blk = threadIdx.x; blk < SM::NCB - 1; blk += T) {
-    int mx = INT_MIN;
+  static_assert(SM::NCB <= 2 * T && S / D <= T - 32, "block-table work split");
+  // This section runs between the stage's two CTA barriers, so its critical path (the busiest
+  // thread) is what the CTA waits for. Column pair c = blocks c and c+1 (the columns
+  // [cD, cD + 2D - 1) one thread's block touches): each thread reduces ONE aligned block of D
+  // words and takes its neighbour's from the next lane (lane 31 reduces the neighbour itself);
+  // a second round covers blocks T .. NCB-1. Row blocks go to warp 1, which has no second round.
+  const int t = threadIdx.x, lane = t & 31;
+  auto block = [&](int blk, int& tm, int& hm) {
+    tm = INT_MIN;
+    hm = 0;
+    if (blk >= SM::NCB) return;
+    const int q = G::pad((X0 + blk * D) % G::RING);
 #pragma unroll
-    for (int d = 0; d < 2 * D; ++d) {
-      const int x = blk * D + d;
-      if (x < G::NCOL) mx = max(mx, sm.colT[b][G::pad(x)]);
-    }
-    sm.colBM2[b][blk] = mx;
-  }
-  for (int blk = threadIdx.x; blk < S / D; blk += T) {
-    int mx = INT_MIN;
-#pragma unroll
-    for (int d = 0; d < D; ++d) mx = max(mx, sm.rowT[b][blk * D + d]);
-    sm.rowBM[b][blk] = mx;
-  }
-  if constexpr (P::kColScale) {
-    for (int x = threadIdx.x; x < S; x += T)
-      sm.rowIBx[b][x] = inv_bound<VB>(scale_word<VB>(&sm.rowB[b][x]));
-  }
-  if constexpr (SM::ZQ) {
-    for (int blk = threadIdx.x; blk < S / D; blk += T) {
-      int hmax = 0;
-#pragma unroll
-      for (int d = 0; d < D; ++d) hmax = max(hmax, scale_word<VB>(&sm.rowB[b][blk * D + d]));
-      const float ib = inv_bound<VB>(hmax);
-      sm.zrow[b][blk] = make_float2(one_minus_tau_ib(sm.rowBM[b][blk], ib), ib);  // same thread wrote rowBM
-    }
-    {
-      // column blocks c = 0 .. NCB-2 of the stage, each over its two aligned D-blocks (the
-      // columns [cD, cD + 2D - 1) one thread's block touches), from the raw words: no dependency
-      // on other threads. results of this call
-      for (int c = threadIdx.x; c < SM::NCB - 1; c += T) {
-        int hmax = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int q = G::pad((X0 + (c + h) * D) % G::RING);
-#pragma unroll
-          for (int d = 0; d < D; ++d)
-            if ((c + h) * D + d < G::NCOL) hmax = max(hmax, scale_word<VB>(&sm.colB[q + d]));
-        }
-        const float ib = inv_bound<VB>(hmax);
-        sm.zcol[b][c] = make_float2(one_minus_tau_ib(sm.colBM2[b][c], ib), ib);  // same thread
+    for (int d = 0; d < D; ++d) {
+      if (blk * D + d < G::NCOL) {
+        tm = max(tm, sm.colT[b][G::pad(blk * D + d)]);
+        if constexpr (SM::ZQ) hm = max(hm, scale_word<VB>(&sm.colB[q + d]));
       }
     }
+  };
+#pragma unroll
+  for (int base = 0; base < 2 * T; base += T) {
+    if (base >= SM::NCB - 1) break;
+    const int c = base + t;
+    int tm, hm;
+    block(c, tm, hm);
+    int tn = __shfl_down_sync(0xffffffffu, tm, 1);
+    int hn = __shfl_down_sync(0xffffffffu, hm, 1);
+    if (lane == 31) block(c + 1, tn, hn);
+    if (c < SM::NCB - 1) {
+      const int tmax = max(tm, tn);
+      sm.colBM2[b][c] = tmax;
+      if constexpr (SM::ZQ) {
+        const float ib = inv_bound<VB>(max(hm, hn));
+        sm.zcol[b][c] = make_float2(one_minus_tau_ib(tmax, ib), ib);
+      }
+    }
+  }
+  if (t >= 32 && t < 32 + S / D) {
+    const int r = t - 32;
+    int mx = INT_MIN, hmax = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      mx = max(mx, sm.rowT[b][r * D + d]);
+      if constexpr (SM::ZQ) hmax = max(hmax, scale_word<VB>(&sm.rowB[b][r * D + d]));
+    }
+    sm.rowBM[b][r] = mx;
+    if constexpr (SM::ZQ) {
+      const float ib = inv_bound<VB>(hmax);
+      sm.zrow[b][r] = make_float2(one_minus_tau_ib(mx, ib), ib);
+    }
+  }
+  if constexpr (P::kColScale) {
+    for (int x = t; x < S; x += T) sm.rowIBx[b][x] = inv_bound<VB>(scale_word<VB>(&sm.rowB[b][x]));
   }
 }
 
