@@ -75,3 +75,29 @@ def test_extension_edge_cases(mp):
     st2 = mp.build_engine_state(mp.make_time_series([0, 0, 0, 1]), mp.ProfileConfig(2, mp.DistanceKind.euclidean()))
     g2 = mp.extend_profile(st2, [0.0])
     assert np.allclose(g2.profile.distances, [0, 0, 1, 1], atol=1e-12)
+
+
+def test_extension_exact_and_fp32_modes(mp):
+    """The extension honours the parity build (exact, refresh_interval) and the FP32 mode: parity
+    vs the oracle for exact, genuine pairs within the FP32 bound for FP32."""
+    r = np.random.default_rng(12)
+    t = 100 + np.cumsum(r.standard_normal(9000))
+    m = 64
+    for fam, p in [(EUCLIDEAN, 2.0), (PNORM, 3.0)]:
+        cfg = mp.ProfileConfig(m, kind(mp, fam, p))
+        cfg.exact, cfg.refresh_interval = True, 256
+        st = mp.extend_profile(mp.build_engine_state(mp.make_time_series(t[:6000]), cfg), t[6000:])
+        _, Pr, Ir = oracle.scan(t, m, fam, p)
+        rep = check(t, m, fam, st.profile.distances, st.profile.nn_index, Pr, Ir, tol=1e-9, p=p)
+        assert rep.ok, rep.summary()
+    for fam, p in [(EUCLIDEAN, 2.0), (ZNORM, 2.0)]:
+        cfg = mp.ProfileConfig(m, kind(mp, fam, p))
+        cfg.precision = mp.Precision.FP32
+        st = mp.extend_profile(mp.build_engine_state(mp.make_time_series(t[:6000]), cfg), t[6000:])
+        I = st.profile.nn_index
+        assert np.all(I >= 0) and np.all(np.abs(I - np.arange(I.size)) >= 1)
+        d = oracle.dist_exact(t, np.arange(I.size), I, m, fam)  # P is the distance of the pair
+        assert np.all(np.abs(st.profile.distances - d) <= 1e-9 * np.maximum(1, d) + (2e-6 if fam == ZNORM else 0))
+        _, P64, _ = oracle.scan(t, m, fam, p)
+        excess = (st.profile.distances - P64) / np.maximum(1, P64)
+        assert excess.max() <= (5e-3 if fam == ZNORM else 1e-4), excess.max()
