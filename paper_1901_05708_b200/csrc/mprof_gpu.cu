@@ -431,6 +431,24 @@ __global__ void k_split(const BestEntry* __restrict__ best, double* __restrict__
 // and near-duplicate z-normalized windows come out at ~1e-14 instead of sqrt(eps). Flat rules
 // as f_value / dist_znorm (acamp.hpp:52-57, oracle.cpp:81-84). In the exact (parity) mode the
 // reference's own conversion of the comparison value is applied.
+// Warp-wide sum over l < m of |a[l] - b[l]|^PK (PK = 0: generic pow), every lane gets the sum.
+template <int PK>
+__device__ __forceinline__ double lane_lp_sum(const double* __restrict__ a, const double* __restrict__ b,
+                                              int m, int lane, double p) {
+  double s = 0.0;
+#pragma unroll 4
+  for (int l = lane; l < m; l += 32) {
+    const double d = fabs(a[l] - b[l]);
+    if constexpr (PK == 2) s = fma(d, d, s);
+    else if constexpr (PK == 1) s += d;
+    else if constexpr (PK == 3) s = fma(d * d, d, s);
+    else if constexpr (PK == 4) { const double d2 = d * d; s = fma(d2, d2, s); }
+    else s += pow(d, p);
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
 __global__ void k_finalize_range(const double* __restrict__ t, const double* __restrict__ cmp,
                                  const int64_t* __restrict__ idx, const double* __restrict__ mu,
                                  const double* __restrict__ B, double* __restrict__ P, int lo, int hi,
@@ -455,6 +473,7 @@ __global__ void k_finalize_range(const double* __restrict__ t, const double* __r
       } else {
         const double mi = mu[i], mj = mu[j];
         double s = 0.0;
+#pragma unroll 4
         for (int l = lane; l < m; l += 32) {
           const double d = (t[i + l] - mi) * bi - (t[j + l] - mj) * bj;
           s = fma(d, d, s);
@@ -463,17 +482,13 @@ __global__ void k_finalize_range(const double* __restrict__ t, const double* __r
         out = sqrt(fmin(md * s, 4.0 * md));
       }
     } else {
-      double s = 0.0;
-      for (int l = lane; l < m; l += 32) {
-        const double d = fabs(t[i + l] - t[j + l]);
-        if (family == MPROF_EUCLIDEAN || p == 2.0) s = fma(d, d, s);
-        else if (p == 1.0) s += d;
-        else if (p == 3.0) s = fma(d * d, d, s);
-        else if (p == 4.0) { const double d2 = d * d; s = fma(d2, d2, s); }
-        else s += pow(d, p);
-      }
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      out = (family == MPROF_EUCLIDEAN || p == 2.0) ? sqrt(s) : (p == 1.0) ? s : pow(s, 1.0 / p);
+      const bool l2 = family == MPROF_EUCLIDEAN || p == 2.0;
+      const double s = l2         ? lane_lp_sum<2>(t + i, t + j, m, lane, p)
+                       : p == 1.0 ? lane_lp_sum<1>(t + i, t + j, m, lane, p)
+                       : p == 3.0 ? lane_lp_sum<3>(t + i, t + j, m, lane, p)
+                       : p == 4.0 ? lane_lp_sum<4>(t + i, t + j, m, lane, p)
+                                  : lane_lp_sum<0>(t + i, t + j, m, lane, p);
+      out = l2 ? sqrt(s) : (p == 1.0) ? s : pow(s, 1.0 / p);
     }
     if (lane == 0) P[i] = out;
   }
