@@ -205,19 +205,29 @@ __global__ void k_bspread(const double* __restrict__ B, int L, double* out) {
 template <class PP>
 __global__ void k_first_diag(SweepParams prm, int k1) {
   using P = typename PP::Base;  // FP64 evaluation, also in FP32 mode
+  // Runs of kRun consecutive cells per thread: a direct length-m seed at the run's first cell,
+  // then the policy's O(1) slide (as the tiles do, over far shorter runs), so the pass costs
+  // ~m/kRun + 3 operations per cell instead of m.
+  constexpr int kRun = 16;
   const int L = prm.L;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + k1 <= L - 1 && i < prm.row_hi;
-       i += gridDim.x * blockDim.x) {
-    const int j = i + k1;
-    const double mui = P::kCenteredSeed ? prm.mu[i] : 0.0;
-    const double muj = P::kCenteredSeed ? prm.mu[j] : 0.0;
+  const int cells = min(L - k1, prm.row_hi);  // cells (i, i + k1), i < cells
+  for (int run = blockIdx.x * blockDim.x + threadIdx.x; run * kRun < cells;
+       run += gridDim.x * blockDim.x) {
+    const int i0 = run * kRun, j0 = i0 + k1;
+    const double mui = P::kCenteredSeed ? prm.mu[i0] : 0.0;
+    const double muj = P::kCenteredSeed ? prm.mu[j0] : 0.0;
     double acc = 0.0;
-    for (int l = 0; l < prm.m; ++l) acc = P::seed(acc, prm.t[i + l] - mui, prm.t[j + l], muj, prm.p);
-    const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
-    const unsigned long long vb =
-        (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
-    offer(prm.best, i, vb, out_index(j, prm.rl));
-    offer(prm.best, j, vb, out_index(i, prm.rl));
+    for (int l = 0; l < prm.m; ++l) acc = P::seed(acc, prm.t[i0 + l] - mui, prm.t[j0 + l], muj, prm.p);
+    const int end = min(kRun, cells - i0);
+    for (int q = 0; q < end; ++q) {
+      const int i = i0 + q, j = j0 + q;
+      if (q > 0) acc = P::step(acc, prm.A[i - 1], prm.A[j - 1], prm.p);
+      const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
+      const unsigned long long vb =
+          (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+      offer(prm.best, i, vb, out_index(j, prm.rl));
+      offer(prm.best, j, vb, out_index(i, prm.rl));
+    }
   }
 }
 
@@ -831,7 +841,7 @@ constexpr int min_blocks() {
 template <class P>
 int32_t launch_first_diag(mprof_ctx* c, const SweepParams& prm, int k1, uint32_t* launches) {
   if (k1 > prm.L - 1) return MPROF_OK;
-  k_first_diag<P><<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);
+  k_first_diag<P><<<grid_for((prm.L - k1 + 15) / 16), 256, 0, c->stream>>>(prm, k1);
   CK(cudaGetLastError());
   ++*launches;
   return MPROF_OK;
