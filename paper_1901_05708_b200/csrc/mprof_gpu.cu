@@ -205,19 +205,36 @@ __global__ void k_bspread(const double* __restrict__ B, int L, double* out) {
 template <class PP>
 __global__ void k_first_diag(SweepParams prm, int k1) {
   using P = typename PP::Base;  // FP64 evaluation, also in FP32 mode
-  // Runs of kRun consecutive cells per thread: a direct length-m seed at the run's first cell,
-  // then the policy's O(1) slide (as the tiles do, over far shorter runs), so the pass costs
-  // ~m/kRun + 3 operations per cell instead of m.
+  // Runs of kRun consecutive cells (i, i + k1) per thread: a direct length-m seed at the run's
+  // first cell, then the policy's O(1) slide (as the tiles do, over far shorter runs). No
+  // atomics: this pass runs alone on the profile, the row entry i of cell i is written only by
+  // its cell's thread (lexicographic min with what is there: +inf, a pinned flat window, or the
+  // previous profile of an extension), and the column entries i + k1 are merged by
+  // k_first_diag_cols from the cell values left in prm.scratch.
   constexpr int kRun = 16;
   const int L = prm.L;
   const int cells = min(L - k1, prm.row_hi);  // cells (i, i + k1), i < cells
-  for (int run = blockIdx.x * blockDim.x + threadIdx.x; run * kRun < cells;
-       run += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nruns = (cells + kRun - 1) / kRun;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  // a warp takes 32 runs: their seeds are computed cooperatively (lanes stride over l, coalesced
+  // loads; the fast mode's seeds need not follow the reference's summation order), then every
+  // lane slides its own run
+  for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < nruns; base += warps * 32) {
+    double mine = 0.0;
+    for (int r = 0; r < 32 && base + r < nruns; ++r) {
+      const int i0 = (base + r) * kRun, j0 = i0 + k1;
+      const double mui = P::kCenteredSeed ? prm.mu[i0] : 0.0;
+      const double muj = P::kCenteredSeed ? prm.mu[j0] : 0.0;
+      double part = 0.0;
+      for (int l = lane; l < prm.m; l += 32) part = P::seed(part, prm.t[i0 + l] - mui, prm.t[j0 + l], muj, prm.p);
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      if (lane == r) mine = part;
+    }
+    const int run = base + lane;
+    if (run >= nruns) continue;
     const int i0 = run * kRun, j0 = i0 + k1;
-    const double mui = P::kCenteredSeed ? prm.mu[i0] : 0.0;
-    const double muj = P::kCenteredSeed ? prm.mu[j0] : 0.0;
-    double acc = 0.0;
-    for (int l = 0; l < prm.m; ++l) acc = P::seed(acc, prm.t[i0 + l] - mui, prm.t[j0 + l], muj, prm.p);
+    double acc = mine;
     const int end = min(kRun, cells - i0);
     for (int q = 0; q < end; ++q) {
       const int i = i0 + q, j = j0 + q;
@@ -225,9 +242,23 @@ __global__ void k_first_diag(SweepParams prm, int k1) {
       const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
       const unsigned long long vb =
           (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
-      offer(prm.best, i, vb, out_index(j, prm.rl));
-      offer(prm.best, j, vb, out_index(i, prm.rl));
+      prm.scratch[i] = __longlong_as_double(static_cast<long long>(vb));
+      const BestEntry cur = prm.best[i];
+      const long long jo = out_index(j, prm.rl);
+      if (lex_less(vb, jo, cur.v, cur.idx)) prm.best[i] = BestEntry{vb, jo};
     }
+  }
+}
+
+// Column side of the first-diagonal pass: entry j takes cell (j - k1, j).
+__global__ void k_first_diag_cols(SweepParams prm, int k1) {
+  const int cells = min(prm.L - k1, prm.row_hi);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cells; i += gridDim.x * blockDim.x) {
+    const int j = i + k1;
+    const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(prm.scratch[i]));
+    const BestEntry cur = prm.best[j];
+    const long long io = out_index(i, prm.rl);
+    if (lex_less(vb, io, cur.v, cur.idx)) prm.best[j] = BestEntry{vb, io};
   }
 }
 
@@ -638,6 +669,7 @@ struct Workspace {
   float2* A32;
   float* B32;
   double* scalars;  // [0] series mean (FP32 offset)
+  double* cv;       // first-diagonal cell values (prepass scratch)
 };
 
 int32_t carve(mprof_ctx* c, int L, Workspace* w) {
@@ -648,7 +680,7 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   const size_t nA32 = align_up(sizeof(float2) * (size_t)L);
   const size_t nB32 = align_up(sizeof(float) * (size_t)L);
   const size_t nS = align_up(8 * sizeof(double));
-  const int32_t st = ensure(&c->ws, &c->ws_bytes, nA + 2 * nB + nBest + nC + nA32 + nB32 + nS);
+  const int32_t st = ensure(&c->ws, &c->ws_bytes, nA + 3 * nB + nBest + nC + nA32 + nB32 + nS);
   if (st != MPROF_OK) return st;
   char* base = static_cast<char*>(c->ws);
   w->A = reinterpret_cast<double2*>(base);
@@ -659,6 +691,7 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   w->A32 = reinterpret_cast<float2*>(base + nA + 2 * nB + nBest + nC);
   w->B32 = reinterpret_cast<float*>(base + nA + 2 * nB + nBest + nC + nA32);
   w->scalars = reinterpret_cast<double*>(base + nA + 2 * nB + nBest + nC + nA32 + nB32);
+  w->cv = reinterpret_cast<double*>(base + nA + 2 * nB + nBest + nC + nA32 + nB32 + nS);
   return MPROF_OK;
 }
 
@@ -841,9 +874,10 @@ constexpr int min_blocks() {
 template <class P>
 int32_t launch_first_diag(mprof_ctx* c, const SweepParams& prm, int k1, uint32_t* launches) {
   if (k1 > prm.L - 1) return MPROF_OK;
-  k_first_diag<P><<<grid_for((prm.L - k1 + 15) / 16), 256, 0, c->stream>>>(prm, k1);
+  k_first_diag<P><<<grid_for((prm.L - k1 + 15) / 16, 128), 128, 0, c->stream>>>(prm, k1);  // >= 1 warp per 32 runs
+  k_first_diag_cols<<<grid_for(prm.L - k1), 256, 0, c->stream>>>(prm, k1);
   CK(cudaGetLastError());
-  ++*launches;
+  *launches += 2;
   return MPROF_OK;
 }
 
@@ -1106,6 +1140,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   prm.rl = rl;
   prm.p = cfg->p;
   prm.stats = nullptr;
+  prm.scratch = w.cv;
   const bool want_stats = knobs().stats;
   if (want_stats) {
     CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));

@@ -382,6 +382,7 @@ struct SweepParams {
                           // (sweeps of the time-reversed series, used by the extension)
   double p;
   unsigned long long* stats;  // optional diagnostics (MPROF_STATS): [0] replays [1] offers
+  double* scratch;            // L doubles of scratch (first-diagonal pass)
 };
 
 // Neighbour index as stored in the profile (original coordinates).
