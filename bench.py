@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--m", type=int, default=M_C4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--merge", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: fused peer-memory merge (default) or the two-ncclMin baseline")
     return ap.parse_args()
 
 
@@ -210,8 +212,8 @@ def main():
     import torch.distributed as dist
     import paper_1901_05708_b200 as mp
     from paper_1901_05708_b200 import workloads as W
-    from paper_1901_05708_b200.distributed import (band_for_rank, finalize_sharded, merge_min_,
-                                                   shard_size)
+    from paper_1901_05708_b200.distributed import (PeerExchange, band_for_rank, finalize_sharded,
+                                                   merge_min_, shard_size)
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -237,6 +239,15 @@ def main():
                     torch.empty(Lp, dtype=torch.float64, device="cuda")) for e in engines}
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
     stream.synchronize()
+    # N > 1: the fused peer-memory merge (one kernel per rank over CUDA-IPC / NVLink buffers,
+    # stream-ordered NCCL one-word barriers) unless --merge nccl asks for the ncclMin baseline
+    peers = {}
+    if world > 1 and args.merge == "peer":
+        try:
+            peers = {e: PeerExchange(mp, L, ctx=ctx, barrier="nccl") for e in engines}
+        except Exception as ex:  # no IPC / peer access: the ncclMin path still works
+            print(f"[bench] peer merge unavailable ({ex}); using the ncclMin merge", file=sys.stderr)
+            peers = {}
 
     sweep_ms = {e: [] for e in engines}
     ops_per_cell = {}
@@ -247,12 +258,19 @@ def main():
             flush.zero_()  # L2 flush between steps (inputs are L2-resident)
             for e in engines:
                 cmp, idx, P = bufs[e]
-                info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], cmp.data_ptr(),
-                                       idx.data_ptr(), ctx=ctx)
-                if world > 1:
+                if e in peers:
+                    px = peers[e]
+                    info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], px.cmp,
+                                           px.idx, ctx=ctx)
+                    px.merge_finalize(d_t.data_ptr(), n, cfgs[e])
+                elif world > 1:
+                    info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1],
+                                           cmp.data_ptr(), idx.data_ptr(), ctx=ctx)
                     merge_min_(cmp, idx)
                     finalize_sharded(mp, d_t.data_ptr(), n, cmp, idx, cfgs[e], P, ctx=ctx)
                 else:
+                    info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1],
+                                           cmp.data_ptr(), idx.data_ptr(), ctx=ctx)
                     mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
                                        P.data_ptr(), ctx=ctx)
                 if record:
@@ -330,7 +348,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": {"workload": f"C4 {'+'.join(engines)}: n={n}, m={m}, exclusion 1, FP64, "
-                                   f"{'equal-area diagonal bands + ncclMin merge + sharded finalize' if world > 1 else 'single GPU'}",
+                                   f"{('equal-area diagonal bands + fused peer-memory merge/finalize' if peers else 'equal-area diagonal bands + ncclMin merge + sharded finalize') if world > 1 else 'single GPU'}",
                        "n": n, "m": m, "engines": engines, "cells_per_step": total_cells,
                        "l2": "flushed every step (256 MiB memset inside the timed region)",
                        "parallelism": f"diagonal-band dp{world}"},
@@ -338,7 +356,7 @@ def main():
 
     # end to end through the public API: pinned host series in, P and I back to the host
     if not args.no_e2e:
-        line["e2e"] = e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx,
+        line["e2e"] = e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, peers,
                           stream)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(t, m, engines)
@@ -348,7 +366,7 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, stream):
+def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, peers, stream):
     import ctypes as C
     from paper_1901_05708_b200 import distributed as D
     L = n - m + 1
@@ -372,6 +390,14 @@ def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, s
             with torch.cuda.stream(stream):
                 d_t = h_t.to("cuda", non_blocking=True)
                 for e in engines:
+                    if e in peers:
+                        px = peers[e]
+                        mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], px.cmp,
+                                        px.idx, ctx=ctx)
+                        px.merge_finalize(d_t.data_ptr(), n, cfgs[e])
+                        h_P.copy_(px.tensor("P"), non_blocking=True)
+                        h_I.copy_(px.tensor("I"), non_blocking=True)
+                        continue
                     cmp = torch.empty(L, dtype=torch.float64, device="cuda")
                     idx = torch.empty(L, dtype=torch.int64, device="cuda")
                     P = torch.empty(world * D.shard_size(L, world), dtype=torch.float64,
@@ -402,7 +428,8 @@ def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, s
     return {"value": total / el, "unit": UNIT, "h2d_bytes_per_step": 8 * n * len(engines),
             "d2h_bytes_per_step": 16 * L * len(engines),
             "path": "C ABI host entry points mprof_aamp / mprof_acamp (pinned host buffers)"
-                    if world == 1 else "mprof_sweep_device + ncclMin merge + sharded mprof_finalize_range_device + all-gather, H2D/D2H pinned",
+                    if world == 1 else ("mprof_sweep_device + fused peer-memory merge/finalize (mprof_merge_finalize_peers), H2D/D2H pinned"
+                                        if peers else "mprof_sweep_device + ncclMin merge + sharded mprof_finalize_range_device + all-gather, H2D/D2H pinned"),
             "ms_per_step": el / args.steps * 1e3}
 
 

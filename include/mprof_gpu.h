@@ -181,6 +181,38 @@ int32_t mprof_finalize_range_device(mprof_ctx* ctx, const double* d_t, uint64_t 
 int32_t mprof_merge_device(mprof_ctx* ctx, double* d_cmp, int64_t* d_idx,
                            const double* d_other_cmp, const int64_t* d_other_idx, uint64_t L);
 
+/* ---- several processes, several GPUs: fused merge over peer memory ------------------------ */
+/* One process per GPU (torch.distributed plumbing): each rank sweeps its band into buffers it
+ * allocated with mprof_ipc_alloc, the ranks exchange the 64-byte handles (any host channel) and
+ * map each other's buffers with mprof_ipc_open (NVLink peer memory; also works between two
+ * processes on one GPU). After a host barrier (every partial complete), rank g calls
+ * mprof_merge_finalize_peers on its slice [lo, hi): one kernel loads the W partial (cmp, idx)
+ * entries over NVLink, takes their lexicographic minimum (MinBuffer::absorb,
+ * /root/reference/proj/src/detail/diag_scan.hpp:45-52), finalizes the distance (as
+ * mprof_finalize_range_device) and stores (P, I) into every rank's output buffers. After a
+ * second barrier every rank holds the whole profile: this replaces the ncclMin all-reduces,
+ * the separate finalize and the all-gather (the scan_diagonals merge of
+ * /root/reference/proj/src/detail/diag_scan.hpp:228-256 across processes). */
+#define MPROF_MAX_PEERS 16
+typedef struct mprof_ipc_handle {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} mprof_ipc_handle;
+/* bytes of device memory on the context's device (cudaMalloc, zero-filled) and its handle. */
+int32_t mprof_ipc_alloc(mprof_ctx* ctx, uint64_t bytes, void** d_ptr, mprof_ipc_handle* handle);
+int32_t mprof_ipc_free(mprof_ctx* ctx, void* d_ptr);
+/* Maps another process's allocation; BadArg for a handle of this process's own allocation. */
+int32_t mprof_ipc_open(mprof_ctx* ctx, const mprof_ipc_handle* handle, void** d_ptr);
+int32_t mprof_ipc_close(mprof_ctx* ctx, void* d_ptr);
+/* nin partial profiles (peer_cmp[r], peer_idx[r], each L entries) -> entries [lo, hi) of the
+ * merged, finalized (P, I) written into nout output buffer pairs (out_P[r], out_I[r], each L
+ * entries, indexed absolutely). 1 <= nin, nout <= MPROF_MAX_PEERS. Asynchronous on the context's
+ * stream. */
+int32_t mprof_merge_finalize_peers(mprof_ctx* ctx, const double* d_t, uint64_t n,
+                                   const mprof_config* cfg, const double* const* peer_cmp,
+                                   const int64_t* const* peer_idx, uint32_t nin,
+                                   double* const* out_P, int64_t* const* out_I, uint32_t nout,
+                                   uint64_t lo, uint64_t hi);
+
 /* ---- streaming extension: EngineState ---------------------------------------------------- */
 /* build_engine_state / extend_profile (/root/reference/proj/include/mprof/engine_state.hpp:26-52,
  * /root/reference/proj/src/engine_state.cpp:11-156). The state keeps the series and the

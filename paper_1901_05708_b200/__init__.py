@@ -31,7 +31,8 @@ __all__ = [
     "profile_length", "default_flat_threshold", "MatrixProfile", "RunInfo", "aamp",
     "aamp_pnorm", "acamp", "sweep_device", "finalize_device", "merge_device", "band_cuts",
     "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context", "EngineState",
-    "build_engine_state", "extend_profile", "brute_profile",
+    "build_engine_state", "extend_profile", "brute_profile", "ipc_alloc", "ipc_free",
+    "ipc_open", "ipc_close", "merge_finalize_peers",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libmprof_gpu.so"
@@ -264,7 +265,18 @@ EXPORTS = {
                                      C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "mprof_profile_multi": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_int32, C.c_void_p, C.c_uint64,
                                         C.POINTER(_Config), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mprof_ipc_alloc": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]),
+    "mprof_ipc_free": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "mprof_ipc_open": (C.c_int32, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mprof_ipc_close": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "mprof_merge_finalize_peers": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64,
+                                               C.POINTER(_Config), C.POINTER(C.c_void_p),
+                                               C.POINTER(C.c_void_p), C.c_uint32,
+                                               C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                               C.c_uint32, C.c_uint64, C.c_uint64]),
 }
+IPC_HANDLE_BYTES = 64
+MAX_PEERS = 16
 PROGRESS_FN = C.CFUNCTYPE(C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p)
 
 _lib = None
@@ -478,6 +490,44 @@ def merge_device(d_cmp: int, d_idx: int, d_ocmp: int, d_oidx: int, L: int,
                  ctx: Optional[Context] = None) -> None:
     _raise(lib().mprof_merge_device(_ctx_handle(ctx), C.c_void_p(d_cmp), C.c_void_p(d_idx),
                                     C.c_void_p(d_ocmp), C.c_void_p(d_oidx), L))
+
+
+def ipc_alloc(nbytes: int, ctx: Optional[Context] = None) -> tuple[int, bytes]:
+    """Device buffer (zero-filled) that other processes can map: (pointer, 64-byte handle)."""
+    ptr = C.c_void_p()
+    h = (C.c_ubyte * IPC_HANDLE_BYTES)()
+    _raise(lib().mprof_ipc_alloc(_ctx_handle(ctx), nbytes, C.byref(ptr), h))
+    return int(ptr.value), bytes(h)
+
+
+def ipc_free(ptr: int, ctx: Optional[Context] = None) -> None:
+    _raise(lib().mprof_ipc_free(_ctx_handle(ctx), C.c_void_p(ptr)))
+
+
+def ipc_open(handle: bytes, ctx: Optional[Context] = None) -> int:
+    """Maps another process's ipc_alloc buffer (NVLink peer memory) into this process."""
+    if len(handle) != IPC_HANDLE_BYTES:
+        raise Error(ErrorCode.BadArgument, "IPC handles are 64 bytes")
+    h = (C.c_ubyte * IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    ptr = C.c_void_p()
+    _raise(lib().mprof_ipc_open(_ctx_handle(ctx), h, C.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int, ctx: Optional[Context] = None) -> None:
+    _raise(lib().mprof_ipc_close(_ctx_handle(ctx), C.c_void_p(ptr)))
+
+
+def merge_finalize_peers(d_t: int, n: int, cfg: ProfileConfig, peer_cmp: Sequence[int],
+                         peer_idx: Sequence[int], out_P: Sequence[int], out_I: Sequence[int],
+                         lo: int, hi: int, ctx: Optional[Context] = None) -> None:
+    """Entries [lo, hi) of the merged + finalized profile of the partials (peer_cmp[r],
+    peer_idx[r]) stored into every (out_P[r], out_I[r]) (peer pointers; one fused kernel)."""
+    c = _to_c(cfg)
+    arr = lambda xs: (C.c_void_p * max(1, len(xs)))(*[C.c_void_p(x) for x in xs])  # noqa: E731
+    _raise(lib().mprof_merge_finalize_peers(_ctx_handle(ctx), C.c_void_p(d_t), n, C.byref(c),
+                                            arr(peer_cmp), arr(peer_idx), len(peer_cmp),
+                                            arr(out_P), arr(out_I), len(out_P), lo, hi))
 
 
 def band_cuts(n: int, m: int, exclusion: int, parts: int) -> list:

@@ -490,15 +490,13 @@ __device__ __forceinline__ double lane_lp_sum(const double* __restrict__ a, cons
   return s;
 }
 
-__global__ void k_finalize_range(const double* __restrict__ t, const double* __restrict__ cmp,
-                                 const int64_t* __restrict__ idx, const double* __restrict__ mu,
-                                 const double* __restrict__ B, double* __restrict__ P, int lo, int hi,
-                                 int m, int family, double p, int exact) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < hi; i += warps) {
-    const double v = cmp[i];
-    const long long j = idx[i];
+// Distance of entry i from its comparison value v and neighbour j, computed by one warp (every
+// lane returns it).
+__device__ __forceinline__ double finalize_entry(const double* __restrict__ t,
+                                                 const double* __restrict__ mu,
+                                                 const double* __restrict__ B, int i, double v,
+                                                 long long j, int lane, int m, int family,
+                                                 double p, int exact) {
     const double md = (double)m;
     double out;
     if (isinf(v) || j < 0) {
@@ -531,7 +529,64 @@ __global__ void k_finalize_range(const double* __restrict__ t, const double* __r
                                   : lane_lp_sum<0>(t + i, t + j, m, lane, p);
       out = l2 ? sqrt(s) : (p == 1.0) ? s : pow(s, 1.0 / p);
     }
+    return out;
+}
+
+__global__ void k_finalize_range(const double* __restrict__ t, const double* __restrict__ cmp,
+                                 const int64_t* __restrict__ idx, const double* __restrict__ mu,
+                                 const double* __restrict__ B, double* __restrict__ P, int lo, int hi,
+                                 int m, int family, double p, int exact) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < hi; i += warps) {
+    const double out = finalize_entry(t, mu, B, i, cmp[i], idx[i], lane, m, family, p, exact);
     if (lane == 0) P[i] = out;
+  }
+}
+
+// Fused multi-process merge + finalize + all-gather over peer memory (CUDA IPC / NVLink): one
+// warp per entry i of [lo, hi); lane r < nin loads rank r's partial (cmp, idx)[i] (peer loads,
+// in parallel), a warp shuffle takes the lexicographic (value, index) minimum (MinBuffer::absorb,
+// /root/reference/proj/src/detail/diag_scan.hpp:45-52; the same rule as k_merge), the warp
+// finalizes the entry, and lane r < nout stores (P, I)[i] into rank r's output buffers (peer
+// stores). Replaces the two ncclMin all-reduces + the finalize + the all-gather.
+struct PeerSet {
+  const double* cmp[MPROF_MAX_PEERS];
+  const int64_t* idx[MPROF_MAX_PEERS];
+  double* P[MPROF_MAX_PEERS];
+  int64_t* I[MPROF_MAX_PEERS];
+  int nin, nout;
+};
+
+__global__ void k_merge_finalize_peers(const double* __restrict__ t, const PeerSet ps,
+                                       const double* __restrict__ mu, const double* __restrict__ B,
+                                       int lo, int hi, int m, int family, double p, int exact) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < hi; i += warps) {
+    double v = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+    long long j = -1;
+    if (lane < ps.nin) {
+      v = ps.cmp[lane][i];
+      j = ps.idx[lane][i];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+      const long long oj = __shfl_xor_sync(0xffffffffu, j, off);
+      // k_merge's rule, made symmetric so every lane ends with the same pair: smaller value,
+      // then smaller index; an untouched entry (-1) loses to any index at an equal value
+      const bool take = ov < v || (ov == v && (j < 0 || (oj >= 0 && oj < j)));
+      if (take) {
+        v = ov;
+        j = oj;
+      }
+    }
+    const double out = finalize_entry(t, mu, B, i, v, j, lane, m, family, p, exact);
+    if (lane < ps.nout) {
+      ps.P[lane][i] = out;
+      ps.I[lane][i] = j;
+    }
   }
 }
 
@@ -1501,6 +1556,100 @@ int32_t mprof_finalize_range_device(mprof_ctx* in, const double* d_t, uint64_t n
   k_finalize_range<<<grid_for(32LL * (long long)(hi - lo)), 256, 0, c->stream>>>(
       d_t, d_cmp, d_idx, w.mu, w.B, d_P, (int)lo, (int)hi, (int)cfg->m, cfg->family, cfg->p,
       cfg->exact ? 1 : 0);
+  CK(cudaGetLastError());
+  return MPROF_OK;
+}
+
+int32_t mprof_ipc_alloc(mprof_ctx* in, uint64_t bytes, void** d_ptr, mprof_ipc_handle* h) {
+  if (!d_ptr || !h || bytes == 0) return fail(MPROF_E_BAD_ARG, "null argument or zero size");
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(mprof_ipc_handle), "IPC handle size");
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return fail(MPROF_E_OOM, "cudaMalloc(%llu) failed", (unsigned long long)bytes);
+  CK(cudaMemset(p, 0, bytes));
+  cudaIpcMemHandle_t ih;
+  if (cudaIpcGetMemHandle(&ih, p) != cudaSuccess) {
+    cudaFree(p);
+    return fail(MPROF_E_CUDA, "cudaIpcGetMemHandle failed");
+  }
+  memcpy(h->bytes, &ih, sizeof(ih));
+  *d_ptr = p;
+  return MPROF_OK;
+}
+
+int32_t mprof_ipc_free(mprof_ctx* in, void* d_ptr) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  CK(cudaFree(d_ptr));
+  return MPROF_OK;
+}
+
+int32_t mprof_ipc_open(mprof_ctx* in, const mprof_ipc_handle* h, void** d_ptr) {
+  if (!h || !d_ptr) return fail(MPROF_E_BAD_ARG, "null argument");
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  cudaIpcMemHandle_t ih;
+  memcpy(&ih, h->bytes, sizeof(ih));
+  const cudaError_t e = cudaIpcOpenMemHandle(d_ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+  if (e == cudaErrorInvalidValue || e == cudaErrorInvalidResourceHandle || e == cudaErrorDeviceUninitialized) {
+    cudaGetLastError();
+    return fail(MPROF_E_BAD_ARG, "cudaIpcOpenMemHandle: %s (own or stale handle?)", cudaGetErrorString(e));
+  }
+  CK(e);
+  return MPROF_OK;
+}
+
+int32_t mprof_ipc_close(mprof_ctx* in, void* d_ptr) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  CK(cudaIpcCloseMemHandle(d_ptr));
+  return MPROF_OK;
+}
+
+int32_t mprof_merge_finalize_peers(mprof_ctx* in, const double* d_t, uint64_t n,
+                                   const mprof_config* cfg, const double* const* peer_cmp,
+                                   const int64_t* const* peer_idx, uint32_t nin,
+                                   double* const* out_P, int64_t* const* out_I, uint32_t nout,
+                                   uint64_t lo, uint64_t hi) {
+  if (!d_t || !cfg || !peer_cmp || !peer_idx || !out_P || !out_I)
+    return fail(MPROF_E_BAD_ARG, "null argument");
+  if (nin < 1 || nin > MPROF_MAX_PEERS || nout < 1 || nout > MPROF_MAX_PEERS)
+    return fail(MPROF_E_BAD_ARG, "peer counts must be in [1, %d]", MPROF_MAX_PEERS);
+  PeerSet ps{};
+  for (uint32_t r = 0; r < nin; ++r) {
+    if (!peer_cmp[r] || !peer_idx[r]) return fail(MPROF_E_BAD_ARG, "null peer buffer %u", r);
+    ps.cmp[r] = peer_cmp[r];
+    ps.idx[r] = peer_idx[r];
+  }
+  for (uint32_t r = 0; r < nout; ++r) {
+    if (!out_P[r] || !out_I[r]) return fail(MPROF_E_BAD_ARG, "null output buffer %u", r);
+    ps.P[r] = out_P[r];
+    ps.I[r] = out_I[r];
+  }
+  ps.nin = (int)nin;
+  ps.nout = (int)nout;
+  int32_t st = check_config(n, cfg);
+  if (st != MPROF_OK) return st;
+  const uint64_t L = n - cfg->m + 1;
+  if (hi > L) hi = L;
+  if (lo >= hi) return MPROF_OK;
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  Workspace w;
+  st = carve(c, (int)L, &w);
+  if (st != MPROF_OK) return st;
+  if (cfg->family == MPROF_ZNORMALIZED) {
+    st = ensure_znorm_stats(c, d_t, n, cfg, w);
+    if (st != MPROF_OK) return st;
+  }
+  k_merge_finalize_peers<<<grid_for(32LL * (long long)(hi - lo)), 256, 0, c->stream>>>(
+      d_t, ps, w.mu, w.B, (int)lo, (int)hi, (int)cfg->m, cfg->family, cfg->p, cfg->exact ? 1 : 0);
   CK(cudaGetLastError());
   return MPROF_OK;
 }

@@ -9,6 +9,11 @@ the final MinBuffer::absorb (diag_scan.hpp:45-52), done here as two all-reduce(M
 which reproduces the lexicographic (value, index) minimum exactly. The finalize (distance of each
 chosen pair recomputed directly) is split the same way: rank g converts entries
 shard_range(L, g, world) with mprof_finalize_range_device and the slices are all-gathered.
+
+PeerExchange is the fused alternative (the default of bench.py): the partial profiles live in
+CUDA-IPC buffers every rank maps, and ONE kernel per rank (mprof_merge_finalize_peers) loads
+the W partials of its slice over NVLink, merges, finalizes and stores the slice of (P, I)
+straight into every rank's output buffers — no ncclMin, no separate finalize, no all-gather.
 """
 from __future__ import annotations
 
@@ -75,3 +80,80 @@ def finalize_sharded(mp, d_t: int, n: int, cmp: torch.Tensor, idx: torch.Tensor,
     mp.finalize_range_device(d_t, n, cmp.data_ptr(), idx.data_ptr(), cfg, P.data_ptr(), lo, hi,
                              ctx=ctx)
     gather_shards_(P, group)
+
+
+class PeerExchange:
+    """Per-rank partial (cmp, idx) and output (P, I) buffers of L entries, allocated with
+    mprof_ipc_alloc and mapped by every other rank (handles exchanged with all_gather_object).
+
+    merge_finalize() runs after this rank's sweep wrote `cmp`/`idx`; afterwards `P`/`I` of EVERY
+    rank hold the merged, finalized profile. Cross-rank ordering: barrier="nccl" uses a
+    one-element all-reduce on the current stream as a stream-ordered barrier (no host sync, one
+    process per GPU); barrier="host" synchronizes the device and calls dist.barrier (gloo, or
+    several processes sharing a GPU, where NCCL cannot run)."""
+
+    def __init__(self, mp, L: int, ctx=None, group=None, barrier: str = "host"):
+        self.mp, self.L, self.ctx, self.group, self.barrier = mp, L, ctx, group, barrier
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > mp.MAX_PEERS:
+            raise ValueError(f"at most {mp.MAX_PEERS} ranks")
+        self.own = {}
+        handles = {}
+        for k in ("cmp", "idx", "P", "I"):
+            self.own[k], handles[k] = mp.ipc_alloc(8 * L, ctx=ctx)
+        allh = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(allh, handles, group=group)
+        else:
+            allh = [handles]
+        self.opened = []
+        self.peer = {k: [] for k in ("cmp", "idx", "P", "I")}
+        for r, h in enumerate(allh):
+            for k in self.peer:
+                if r == self.rank:
+                    ptr = self.own[k]
+                else:
+                    ptr = mp.ipc_open(h[k], ctx=ctx)
+                    self.opened.append(ptr)
+                self.peer[k].append(ptr)
+        self.cmp, self.idx, self.P, self.I = (self.own[k] for k in ("cmp", "idx", "P", "I"))
+
+    def _barrier(self) -> None:
+        if self.world == 1:
+            return
+        if self.barrier == "nccl":
+            import torch
+            if getattr(self, "_flag", None) is None:
+                self._flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            import torch
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def merge_finalize(self, d_t: int, n: int, cfg) -> None:
+        lo, hi = shard_range(self.L, self.rank, self.world)
+        self._barrier()  # every rank's partial is complete
+        self.mp.merge_finalize_peers(d_t, n, cfg, self.peer["cmp"], self.peer["idx"],
+                                     self.peer["P"], self.peer["I"], lo, hi, ctx=self.ctx)
+        self._barrier()  # every slice has landed in every rank's (P, I)
+
+    def tensor(self, name: str):
+        """Zero-copy torch view of this rank's own buffer ("cmp", "idx", "P" or "I")."""
+        import torch
+
+        class _Raw:
+            pass
+        raw = _Raw()
+        raw.__cuda_array_interface__ = {
+            "shape": (self.L,), "typestr": "<i8" if name in ("idx", "I") else "<f8",
+            "data": (self.own[name], False), "version": 2, "strides": None}
+        return torch.as_tensor(raw, device="cuda")
+
+    def close(self) -> None:
+        for ptr in self.opened:
+            self.mp.ipc_close(ptr, ctx=self.ctx)
+        self.opened = []
+        for k in list(self.own):
+            self.mp.ipc_free(self.own.pop(k), ctx=self.ctx)
