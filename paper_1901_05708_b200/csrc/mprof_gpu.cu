@@ -49,6 +49,9 @@ constexpr int kK = kD * kT;
 // least this (calibrated on the BASELINE workloads: m=1024 0.983, m=512 0.967 -> cov-only is
 // faster; m=256 0.93 -> column-scaled is 1.8x faster)
 constexpr double kZnCovFilterMinSpread = 0.955;
+// the same test for the covariance-form AAMP kernel (EuclidCov): measured on random walks,
+// m=1024 (spread 0.983) -10.7 %, m=256 (0.93) -7 %, m=128 +6.5 %, m=100 (C1) 3.9x slower
+constexpr double kAampCovMinSpread = 0.92;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
@@ -59,6 +62,7 @@ struct Knobs {
   int zn_filter = 0;            // MPROF_ZN_FILTER=cov|col: force the z-norm filter form
   bool zn_no_near = false;      // MPROF_ZN_NO_NEAR: no column-scaled near-diagonal block
   bool stats = false;           // MPROF_STATS: count replays / offers (stderr)
+  int aamp_cov = -1;            // MPROF_AAMP_COV=0|1: force the AAMP form (-1: by window spread)
 };
 const Knobs& knobs() {
   static const Knobs k = [] {
@@ -69,6 +73,7 @@ const Knobs& knobs() {
     if (const char* e = getenv("MPROF_ZN_FILTER")) r.zn_filter = !strcmp(e, "cov") ? 1 : !strcmp(e, "col") ? 2 : 0;
     r.zn_no_near = getenv("MPROF_ZN_NO_NEAR") != nullptr;
     r.stats = getenv("MPROF_STATS") != nullptr;
+    if (const char* e = getenv("MPROF_AAMP_COV")) r.aamp_cov = atoi(e) ? 1 : 0;
     return r;
   }();
   return k;
@@ -136,6 +141,30 @@ __global__ void k_znorm_stats(const double* __restrict__ t, int L, int m, double
     mu[p] = mean;
     const double var = ss / m;
     B[p] = (var <= flat_thr) ? 0.0 : 1.0 / sqrt(ss);
+  }
+}
+
+// Covariance-form AAMP statistics (EuclidCov in sweep.cuh): two-pass window mean mu_p and
+// centred sum of squares S_p (FP64, exact inputs of the comparison values), the float ring
+// scalars SB[p] = {S_p rounded down, mu_p - t[0] rounded down} of the filter tables, and
+// Bq[p] = 1/sqrt(S_p) (0 for a constant window) for the spread test (k_bspread).
+__global__ void k_euclid_stats(const double* __restrict__ t, int L, int m, double* __restrict__ mu,
+                               double* __restrict__ S, float2* __restrict__ SB,
+                               double* __restrict__ Bq) {
+  const double t0 = t[0];
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < m; ++l) s += t[p + l] - t0;
+    const double mean0 = s / m;  // mean of t - t[0]: keeps the digits of level-offset series
+    double ss = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double d = (t[p + l] - t0) - mean0;
+      ss = fma(d, d, ss);
+    }
+    mu[p] = mean0 + t0;
+    S[p] = ss;
+    SB[p] = make_float2(__double2float_rd(ss), __double2float_rd(mean0));
+    Bq[p] = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
   }
 }
 
@@ -654,6 +683,7 @@ struct mprof_ctx {
   uint64_t stats_n = 0, stats_m = 0;
   double stats_thr = -1.0;
   bool zn_colscale = false;  // z-norm filter form chosen for the current sweep
+  bool aamp_cov = false;     // AAMP form chosen for the current sweep (covariance vs delta-sigma)
   double* d_spread = nullptr;
   mprof_progress_fn progress = nullptr;  // anytime observer (band granularity)
   void* progress_user = nullptr;
@@ -725,6 +755,11 @@ struct Workspace {
   float* B32;
   double* scalars;  // [0] series mean (FP32 offset)
   double* cv;       // first-diagonal cell values (prepass scratch)
+  // covariance-form AAMP (own arrays: the z-norm statistics above are cached per series)
+  double2* A2;      // (df, dg) operand pairs
+  double* emu;      // window means
+  double* S;        // centred sums of squares
+  float2* SB;       // ring scalars {S rd, mu - t[0] rd}
 };
 
 int32_t carve(mprof_ctx* c, int L, Workspace* w) {
@@ -735,7 +770,8 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   const size_t nA32 = align_up(sizeof(float2) * (size_t)L);
   const size_t nB32 = align_up(sizeof(float) * (size_t)L);
   const size_t nS = align_up(8 * sizeof(double));
-  const int32_t st = ensure(&c->ws, &c->ws_bytes, nA + 3 * nB + nBest + nC + nA32 + nB32 + nS);
+  const int32_t st = ensure(&c->ws, &c->ws_bytes,
+                            nA + 3 * nB + nBest + nC + nA32 + nB32 + nS + nA + 2 * nB + nA32);
   if (st != MPROF_OK) return st;
   char* base = static_cast<char*>(c->ws);
   w->A = reinterpret_cast<double2*>(base);
@@ -747,6 +783,11 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   w->B32 = reinterpret_cast<float*>(base + nA + 2 * nB + nBest + nC + nA32);
   w->scalars = reinterpret_cast<double*>(base + nA + 2 * nB + nBest + nC + nA32 + nB32);
   w->cv = reinterpret_cast<double*>(base + nA + 2 * nB + nBest + nC + nA32 + nB32 + nS);
+  char* e = base + nA + 3 * nB + nBest + nC + nA32 + nB32 + nS;
+  w->A2 = reinterpret_cast<double2*>(e);
+  w->emu = reinterpret_cast<double*>(e + nA);
+  w->S = reinterpret_cast<double*>(e + nA + nB);
+  w->SB = reinterpret_cast<float2*>(e + nA + 2 * nB);
   return MPROF_OK;
 }
 
@@ -979,6 +1020,7 @@ int32_t with_policy(const mprof_ctx* c, const mprof_config* cfg, F&& f) {
   if (cfg->family == MPROF_ZNORMALIZED)
     return c->zn_colscale ? f.template operator()<Znorm<true>>() : f.template operator()<Znorm<false>>();
   const bool ex = cfg->exact != 0;
+  if (l2 && !ex && c->aamp_cov) return f.template operator()<EuclidCov>();
   if (l2) return ex ? f.template operator()<Euclid<true>>() : f.template operator()<Euclid<false>>();
   if (p == 1.0) return ex ? f.template operator()<Pnorm<1, true>>() : f.template operator()<Pnorm<1, false>>();
   if (p == 3.0) return ex ? f.template operator()<Pnorm<3, true>>() : f.template operator()<Pnorm<3, false>>();
@@ -1018,8 +1060,10 @@ int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams&
     if (st != MPROF_OK) return st;
     CK(cudaEventRecord(c->ev_fork, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    st = cfg->precision == MPROF_FP32 ? launch_tiles<ZnormF32<true>>(prm, 0, n_near, c->side, launches)
-                                      : launch_tiles<Znorm<true>>(prm, 0, n_near, c->side, launches);
+    // near block: the column-scaled z-norm form, or the (delta, sigma) AAMP kernel
+    if (cfg->family != MPROF_ZNORMALIZED) st = launch_tiles<Euclid<false>>(prm, 0, n_near, c->side, launches);
+    else if (cfg->precision == MPROF_FP32) st = launch_tiles<ZnormF32<true>>(prm, 0, n_near, c->side, launches);
+    else st = launch_tiles<Znorm<true>>(prm, 0, n_near, c->side, launches);
     if (st != MPROF_OK) return st;
     CK(cudaEventRecord(c->ev_join, c->side));
   }
@@ -1118,6 +1162,29 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
                                     (cfg->family == MPROF_PNORM && cfg->p == 2.0));
     k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m, ds ? kPairsDeltaSum : kPairsRaw);
     ++*launches;
+    c->aamp_cov = false;
+    if (ds && cfg->precision == MPROF_FP64 && knobs().aamp_cov != 0) {
+      // covariance form (EuclidCov) when the window scales vary little inside the filter
+      // blocks (the same spread test as the z-norm filter form; MPROF_AAMP_COV=0|1 overrides)
+      k_euclid_stats<<<g, 256, 0, c->stream>>>(d_t, L, m, w.emu, w.S, w.SB, w.cv);
+      ++*launches;
+      bool use = knobs().aamp_cov == 1;
+      if (!use) {
+        if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
+        CK(cudaMemsetAsync(c->d_spread, 0, 2 * sizeof(double), c->stream));
+        k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.cv, L, c->d_spread);
+        double h[2];
+        CK(cudaMemcpyAsync(h, c->d_spread, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        ++*launches;
+        use = h[1] > 0.0 && h[0] / h[1] >= kAampCovMinSpread;
+      }
+      if (use) {
+        k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.emu, w.A2, L, m);
+        ++*launches;
+        c->aamp_cov = true;
+      }
+    }
   }
   if (cfg->precision == MPROF_FP32) {
     if (zn) {
@@ -1163,7 +1230,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     std::memcpy(&pbits, &cfg->p, sizeof pbits);
     const long long key[9] = {L, k_tile, k_hi, row_hi, (long long)cfg->m, cfg->exact,
                               (long long)cfg->refresh_interval,
-                              ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0),
+                              ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) | (c->aamp_cov ? 2 : 0),
                               pbits};
     if (std::equal(key, key + 9, c->R_key)) {
       out->R = c->R_val;
@@ -1183,7 +1250,10 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   prm.B = w.B;
   prm.A32 = w.A32;
   prm.B32 = w.B32;
-  prm.mu = w.mu;
+  prm.mu = c->aamp_cov && cfg->family != MPROF_ZNORMALIZED ? w.emu : w.mu;
+  prm.A2 = w.A2;
+  prm.SB = w.SB;
+  prm.S = w.S;
   prm.best = w.best;
   prm.tiles = c->tiles_d;
   prm.n = n;
@@ -1202,8 +1272,9 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
   }
   long long n_near = 0;
-  if (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale && !cfg->exact &&
-      k_tile <= (int)cfg->exclusion + 1 && !knobs().zn_no_near)
+  const bool cov_main = (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale) ||
+                        (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov);
+  if (cov_main && !cfg->exact && k_tile <= (int)cfg->exclusion + 1 && !knobs().zn_no_near)
     n_near = count_tiles(L, k_tile, std::min(k_tile + kK, k_hi), row_hi, out->R, S);  // first block
   st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
                       &out->ms);
@@ -1238,7 +1309,7 @@ void fill_info(mprof_ctx* c, const mprof_config* cfg, uint64_t cells, long long 
   float ops = 4.f;
   if (cfg->family == MPROF_ZNORMALIZED) ops = c->zn_colscale ? 3.125f : 2.f;
   else if (cfg->exact) ops = (cfg->family == MPROF_PNORM && cfg->p != 1.0 && cfg->p != 2.0) ? 8.f : 6.f;
-  else if (cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0) ops = 3.f;
+  else if (cfg->family == MPROF_EUCLIDEAN || cfg->p == 2.0) ops = c->aamp_cov ? 2.f : 3.f;
   else if (cfg->p == 1.0) ops = 4.f;
   else if (cfg->p == 3.0 || cfg->p == 4.0) ops = 6.f;
   else ops = 0.f;  // generic pow: library call, not a fixed count

@@ -246,6 +246,73 @@ struct Znorm : KeyF64 {
   }
 };
 
+// AAMP in covariance form (fast FP64 mode, long windows): the accumulator is the CENTRED
+// covariance slid exactly as Znorm does (A2[p] = (df_p, dg_p), 2 DFMA per cell), and
+//   D^2(i, j) = S_i + S_j + m (mu_i - mu_j)^2 - 2 cov(i, j),   S_p = ||t_p - mu_p||^2
+// (the well-conditioned split of ||x - y||^2 into centred parts and means). The hot loop keeps
+// only cov: a cell can reach a threshold tau only if 2 cov >= S_i + S_j + m (mu_i - mu_j)^2 - tau,
+// bounded per block from per-stage tables of min S, the mean range and max tau of its rows and
+// column pair (SB[p] = {S_p rounded down, mu_p - t[0] rounded down} as float2 in the rings).
+// Exact comparison values (replays, seed cells) use the FP64 S and mu from global memory. The
+// diagonal block next to the exclusion zone runs the (delta, sigma) kernel (Base) instead: there
+// the neighbours are within the block bound's slack. Replaces EuclidScan's slide
+// (/root/reference/proj/src/diag_scan.cpp:7-24, incremental_euclidean_step aamp.hpp:37-42).
+struct EuclidCov : KeyF64 {
+  using Base = Euclid<false>;
+  using V = double;
+  using V2 = double2;
+  using VB = float2;
+  static constexpr bool kHasB = true;
+  static constexpr bool kCenteredSeed = true;
+  static constexpr bool kCovFilter = true;
+  static constexpr bool kColScale = false;
+  static constexpr bool kEuclidCov = true;
+  static constexpr bool kPairsAlt = true;  // operands in SweepParams::A2
+  static constexpr int kMinWarps = 16;
+  static constexpr int kPairs = kPairsZnorm;
+  __device__ __forceinline__ static double step(double acc, double2 r, double2 c, double) {
+    return fma(r.x, c.y, fma(c.x, r.y, acc));
+  }
+  // a = t_i - mu_i (row, pre-centred), b = t_j, mub = mu_j
+  __device__ __forceinline__ static double seed(double acc, double a, double b, double mub,
+                                                double) {
+    return fma(a, b - mub, acc);
+  }
+  __device__ __forceinline__ static double value(double cov, double si, double sj, double mi,
+                                                 double mj, double md) {
+    const double dm = mi - mj;
+    return fma(md * dm, dm, si + sj) - 2.0 * cov;
+  }
+};
+
+template <class P>
+constexpr bool is_euclid_cov() {
+  if constexpr (requires { P::kEuclidCov; }) return P::kEuclidCov;
+  else return false;
+}
+
+// Exact per-cell inputs of comparison values that are not kept in the rings (EuclidCov): in
+// static shared memory, written once per CTA, so the hot loop keeps no registers for them.
+struct CellCtx {
+  const double* S;
+  const double* mu;
+  double md;
+};
+__shared__ CellCtx g_cell_ctx;
+
+// Comparison value of cell (i, j) from its accumulator.
+template <class P>
+__device__ __forceinline__ double cell_value(typename P::V acc, typename P::VB rb,
+                                             typename P::VB cb, int i, int j) {
+  if constexpr (is_euclid_cov<P>()) {
+    const CellCtx& cc = g_cell_ctx;
+    return P::value(acc, __ldg(cc.S + i), __ldg(cc.S + j), __ldg(cc.mu + i), __ldg(cc.mu + j),
+                    cc.md);
+  } else {
+    return static_cast<double>(P::score(acc, rb, cb));
+  }
+}
+
 // ---- FP32 mode policies ------------------------------------------------------------------------
 // Same slides in float; seeds in FP64 (rounded once to float). Operands are built relative to a
 // global offset c (the series mean) so that float keeps the digits that matter: AAMP
@@ -348,21 +415,30 @@ struct SweepSmem {
   V2 colA[G::RINGP];                           // ring: A[cbase + X] at pad(X mod RING)
   VB colB[HASB ? G::RINGP : 2];                // ring: B[cbase + 1 + X]
   int colT[2][G::NCOLP];                       // hi32(best[i0 + kb + 1 + x].v), exact
-  int colBM2[2][NCB];                          // max of colT over columns [cD, cD + 2D)
+  // Block tables are single-buffered: they are rebuilt between the two barriers of each stage,
+  // when no warp reads them. The covariance forms keep their own tables instead of the max
+  // threshold words.
+  static constexpr bool EQ = is_euclid_cov<P>();
+  static constexpr bool ZQ = P::kCovFilter && !P::kColScale && !EQ;
+  static constexpr bool TW = !(ZQ || EQ);     // filters on threshold words (colBM2 / rowBM)
+  int colBM2[TW ? NCB : 1];                    // max of colT over columns [cD, cD + 2D)
   V2 rowA[2][S];                               // A[i0 + x]
   VB rowB[2][HASB ? S : 2];                    // B[i0 + 1 + x]
   int rowT[2][S];                              // hi32(best[i0 + 1 + x].v), exact
-  int rowBM[2][S / D];                         // max of rowT over aligned blocks of D
+  int rowBM[TW ? S / D : 1];                   // max of rowT over aligned blocks of D
   // z-norm filter scales, rounded DOWN (a smaller scale only loosens the filter).
-  float rowIBx[2][HASB ? S : 1];               // <= 1 / rowB of each row (column-scaled form)
+  float rowIBx[P::kColScale ? S : 1];          // <= 1 / rowB of each row (column-scaled form)
   // Covariance-only z-norm filter, per stage: for row block r, {lower bound of (1 - tau_r) *
   // IB_r, IB_r}; for column block c (covering stage columns [cD, cD + 2D)), {lower bound of
   // (1 - tau_c) * IB_c, IB_c}, tau = max threshold, IB <= 1 / max B of the block; -inf = "some
   // threshold >= 1, every cell may pass". A block's covariance bound is then
   // min(RQ_r * IB_c, CQ_c * IB_r) (= (1 - max(tau_r, tau_c)) * IB_r * IB_c).
-  static constexpr bool ZQ = P::kCovFilter && !P::kColScale;
-  float2 zrow[2][ZQ ? S / D : 1];
-  float2 zcol[2][ZQ ? NCB : 1];
+  float2 zrow[ZQ ? S / D : 1];
+  float2 zcol[ZQ ? NCB : 1];
+  // Covariance-form AAMP filter, per stage: {min S (down), min mu (down), max mu (up),
+  // max tau (up)} of each row block and column block pair.
+  float4 erow[EQ ? S / D : 1];
+  float4 ecol[EQ ? NCB : 1];
 };
 
 struct SweepParams {
@@ -371,7 +447,10 @@ struct SweepParams {
   const double* B;        // FP64 per-position scale (z-norm), valid [0, L)
   const float2* A32;      // FP32 mode operand pairs
   const float* B32;       // FP32 mode scales
-  const double* mu;       // window means (z-norm), valid [0, L)
+  const double* mu;       // window means (z-norm, covariance-form AAMP), valid [0, L)
+  const double2* A2;      // covariance-form AAMP operand pairs (df, dg), valid [0, L-1)
+  const float2* SB;       // covariance-form AAMP ring scalars {S rd, mu - t[0] rd}, valid [0, L)
+  const double* S;        // covariance-form AAMP centred sums of squares, valid [0, L)
   BestEntry* best;        // L entries
   const int4* tiles;      // (first diagonal kb, first row ra, row end re, -) per CTA
   int n, m, L;
@@ -390,12 +469,14 @@ __device__ __forceinline__ int out_index(int idx, int rl) { return rl > 0 ? rl -
 
 template <class P>
 __device__ __forceinline__ const typename P::V2* pairs_of(const SweepParams& prm) {
-  if constexpr (sizeof(typename P::V) == 8) return prm.A;
+  if constexpr (is_euclid_cov<P>()) return prm.A2;
+  else if constexpr (sizeof(typename P::V) == 8) return prm.A;
   else return prm.A32;
 }
 template <class P>
 __device__ __forceinline__ const typename P::VB* scales_of(const SweepParams& prm) {
-  if constexpr (sizeof(typename P::V) == 8) return prm.B;
+  if constexpr (is_euclid_cov<P>()) return prm.SB;
+  else if constexpr (sizeof(typename P::V) == 8) return prm.B;
   else return prm.B32;
 }
 
@@ -465,15 +546,15 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
                                           const typename P::VB* cB2, int* cT1, int* cT2,
                                           const typename P::V2* rowA, const typename P::VB* rowB,
                                           int* rowT, BestEntry* best, unsigned long long* stats) {
-  using V = typename P::V;
   using V2 = typename P::V2;
+  using VB = typename P::VB;
   if (stats) atomicAdd(&stats[0], 1ull);
 #pragma unroll
   for (int u = 0; u < D; ++u) {
     if (GUARD && s + u >= cnt) break;
     const int x = s + u;
     const V2 r = rowA[x];
-    const V rb = P::kHasB ? rowB[x] : V(0);
+    const VB rb = P::kHasB ? rowB[x] : VB{};
     const int row = i0 + x + 1;
     const int tr = *reinterpret_cast<volatile int*>(&rowT[x]);
     unsigned long long rv = kInfBits;
@@ -483,9 +564,9 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
       const int e = u + d;  // entry of the block's column run
       const V2 c = e < D ? cA1[e] : cA2[e - D];
       acc.a[d] = P::step(acc.a[d], r, c, p);
-      const double v = static_cast<double>(
-          P::score(acc.a[d], rb, P::kHasB ? (e < D ? cB1[e] : cB2[e - D]) : V(0)));
       if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) continue;
+      const double v = cell_value<P>(acc.a[d], rb, P::kHasB ? (e < D ? cB1[e] : cB2[e - D]) : VB{},
+                                     row, row + kt + d);
       const int h = __double2hiint(v);
       int* ct = e < D ? &cT1[e] : &cT2[e - D];
       const bool rowhit = h <= tr;
@@ -565,7 +646,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // theta: key bound of the block; num: covariance filters' 1 - tau_max (0 = every cell may pass)
   auto block_theta = [&](int s, int& theta, double& num) {
     const int cb = s / D + threadIdx.x;
-    const int tmax = max(sm.rowBM[b][s / D], sm.colBM2[b][cb]);
+    const int tmax = max(sm.rowBM[s / D], sm.colBM2[cb]);
     theta = P::tau(tmax);
     num = 0.0;
     if constexpr (P::kCovFilter && kColScale) {
@@ -576,11 +657,23 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // Covariance-only form: the stage tables make it two broadcast/strided loads and float math;
   // the bound is kept as a raw word (hit <=> max raw(cov) >= bound), INT_MIN = every cell may
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
-  constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ;
+  constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
+  const float md_f = static_cast<float>(is_euclid_cov<P>() ? g_cell_ctx.md : 0.0);
   auto block_theta_cov = [&](int s) {
-    const float2 rq = sm.zrow[b][s / D];
-    const float2 cq = sm.zcol[b][s / D + threadIdx.x];
-    const float th = fminf(__fmul_rd(rq.x, cq.y), __fmul_rd(cq.x, rq.y));
+    float th;
+    if constexpr (SweepSmem<P, D, T, S>::EQ) {
+      // 2 cov >= S_i + S_j + m (mu_i - mu_j)^2 - tau over the block's rows and columns
+      const float4 rq = sm.erow[s / D];
+      const float4 cq = sm.ecol[s / D + threadIdx.x];
+      const float gap = fmaxf(0.f, fmaxf(__fsub_rd(cq.y, rq.z), __fsub_rd(rq.y, cq.z)));
+      const float ss = __fmaf_rd(__fmul_rd(md_f, gap), gap, __fadd_rd(rq.x, cq.x));
+      // margin for the FP64 roundings of the replay's value (relative to its terms)
+      th = 0.5f * __fsub_rd(__fmul_rd(ss, 1.f - 0x1p-20f), fmaxf(rq.w, cq.w));
+    } else {
+      const float2 rq = sm.zrow[s / D];
+      const float2 cq = sm.zcol[s / D + threadIdx.x];
+      th = fminf(__fmul_rd(rq.x, cq.y), __fmul_rd(cq.x, rq.y));
+    }
     return th > 0.f ? P::cov_bound_raw_f(th) : INT_MIN;
   };
   int theta_nx;
@@ -627,7 +720,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       if constexpr (kColScale) {
         // row bound for this sub-step: cov * B_j >= (1 - tau) / B_i
         const int tu = (num == 0.0) ? INT_MAX
-                                    : P::cov_bound(num * static_cast<double>(sm.rowIBx[b][x]));
+                                    : P::cov_bound(num * static_cast<double>(sm.rowIBx[x]));
         hit |= hu <= tu;
       } else if constexpr (ZQ) {
         hmin = max(hmin, hu);
@@ -673,6 +766,16 @@ __device__ __forceinline__ float one_minus_tau_ib(int tmax, float ib) {
   return u > 0.f ? __fmul_rd(u, ib) : -INFINITY;
 }
 
+// Covariance-form AAMP tables: an upper bound (float) of the comparison values with high word
+// <= w (+inf for the unset threshold), and of a mean stored rounded down.
+__device__ __forceinline__ float tau_up(int w) {
+  if (w >= 0x7FF00000) return INFINITY;
+  return w < 0 ? 0.f : __double2float_ru(__hiloint2double(w, -1));
+}
+__device__ __forceinline__ float mu_up(float v) {
+  return v == -INFINITY ? v : __fadd_ru(v, fmaxf(fabsf(v) * 0x1p-22f, 0x1p-126f));
+}
+
 // Block maxima of the freshly loaded thresholds (after the stage's cp.async completed).
 template <class P, int D, int T, int S>
 __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b, int X0) {
@@ -686,6 +789,58 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
   // words and takes its neighbour's from the next lane (lane 31 reduces the neighbour itself);
   // a second round covers blocks T .. NCB-1. Row blocks go to warp 1, which has no second round.
   const int t = threadIdx.x, lane = t & 31;
+  if constexpr (SM::EQ) {
+    // {min S, min mu, max mu, max tau} per aligned block of D columns; pair c = blocks c, c+1
+    auto block = [&](int blk) {
+      float4 v = make_float4(INFINITY, INFINITY, -INFINITY, 0.f);
+      int tm = INT_MIN;
+      if (blk < SM::NCB) {
+        const int q = G::pad((X0 + blk * D) % G::RING);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          if (blk * D + d < G::NCOL) {
+            tm = max(tm, sm.colT[b][G::pad(blk * D + d)]);
+            const float2 sb = sm.colB[q + d];
+            v.x = fminf(v.x, sb.x);
+            v.y = fminf(v.y, sb.y);
+            v.z = fmaxf(v.z, sb.y);
+          }
+        }
+      }
+      v.w = tau_up(tm);
+      return v;
+    };
+#pragma unroll
+    for (int base = 0; base < 2 * T; base += T) {
+      if (base >= SM::NCB - 1) break;
+      const int c = base + t;
+      const float4 v = block(c);
+      float4 o;
+      o.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+      o.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+      o.z = __shfl_down_sync(0xffffffffu, v.z, 1);
+      o.w = __shfl_down_sync(0xffffffffu, v.w, 1);
+      if (lane == 31) o = block(c + 1);
+      if (c < SM::NCB - 1)
+        sm.ecol[c] = make_float4(fminf(v.x, o.x), fminf(v.y, o.y), mu_up(fmaxf(v.z, o.z)),
+                                 fmaxf(v.w, o.w));
+    }
+    if (t >= 32 && t < 32 + S / D) {
+      const int r = t - 32;
+      float4 v = make_float4(INFINITY, INFINITY, -INFINITY, 0.f);
+      int tm = INT_MIN;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        tm = max(tm, sm.rowT[b][r * D + d]);
+        const float2 sb = sm.rowB[b][r * D + d];
+        v.x = fminf(v.x, sb.x);
+        v.y = fminf(v.y, sb.y);
+        v.z = fmaxf(v.z, sb.y);
+      }
+      sm.erow[r] = make_float4(v.x, v.y, mu_up(v.z), tau_up(tm));
+    }
+    return;
+  }
   auto block = [&](int blk, int& tm, int& hm) {
     tm = INT_MIN;
     hm = 0;
@@ -710,10 +865,10 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
     if (lane == 31) block(c + 1, tn, hn);
     if (c < SM::NCB - 1) {
       const int tmax = max(tm, tn);
-      sm.colBM2[b][c] = tmax;
+      if constexpr (SM::TW) sm.colBM2[c] = tmax;
       if constexpr (SM::ZQ) {
         const float ib = inv_bound<VB>(max(hm, hn));
-        sm.zcol[b][c] = make_float2(one_minus_tau_ib(tmax, ib), ib);
+        sm.zcol[c] = make_float2(one_minus_tau_ib(tmax, ib), ib);
       }
     }
   }
@@ -725,14 +880,14 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
       mx = max(mx, sm.rowT[b][r * D + d]);
       if constexpr (SM::ZQ) hmax = max(hmax, scale_word<VB>(&sm.rowB[b][r * D + d]));
     }
-    sm.rowBM[b][r] = mx;
+    if constexpr (SM::TW) sm.rowBM[r] = mx;
     if constexpr (SM::ZQ) {
       const float ib = inv_bound<VB>(hmax);
-      sm.zrow[b][r] = make_float2(one_minus_tau_ib(mx, ib), ib);
+      sm.zrow[r] = make_float2(one_minus_tau_ib(mx, ib), ib);
     }
   }
   if constexpr (P::kColScale) {
-    for (int x = t; x < S; x += T) sm.rowIBx[b][x] = inv_bound<VB>(scale_word<VB>(&sm.rowB[b][x]));
+    for (int x = t; x < S; x += T) sm.rowIBx[x] = inv_bound<VB>(scale_word<VB>(&sm.rowB[b][x]));
   }
 }
 
@@ -794,6 +949,10 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   const int m = prm.m;
   const int kt = kb + static_cast<int>(threadIdx.x) * D;
   const int kend = min(kb + G::K, prm.k_hi);
+  if constexpr (is_euclid_cov<P>()) {
+    if (threadIdx.x == 0) g_cell_ctx = CellCtx{prm.S, prm.mu, static_cast<double>(m)};
+    __syncthreads();
+  }
 
   // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d) --------------------
   double sacc[D];
@@ -852,13 +1011,13 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
     const VB* Bs = scales_of<P>(prm);
     Cells<D> c;
     unsigned valid = 0;
-    const VB rb = P::kHasB ? Bs[ra] : VB(0);
+    const VB rb = P::kHasB ? Bs[ra] : VB{};
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int k = kt + d;
       const bool ok = (k < kend) && (ra + k <= L - 1);
-      const VB cb = (P::kHasB && ok) ? Bs[ra + k] : VB(0);
-      c.v[d] = static_cast<double>(P::score(acc[d], rb, cb));
+      const VB cb = (P::kHasB && ok) ? Bs[ra + k] : VB{};
+      c.v[d] = ok ? cell_value<P>(acc[d], rb, cb, ra, ra + k) : 0.0;
       valid |= (ok ? 1u : 0u) << d;
     }
     resolve_seed<D>(c, valid, ra, ra + kt, prm.rl, prm.best);
