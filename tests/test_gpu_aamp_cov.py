@@ -48,7 +48,7 @@ def test_cov_form_exact_copies(mp):
     r0 = np.random.default_rng(8)
     t = np.cumsum(r0.standard_normal(14000))
     seg = t[1000:2600].copy()
-    for s in (5000, 9000, 12000):  # three exact copies (after the level shift below)
+    for s in (5000, 9000, 12000):  # three exact copies of the segment
         t[s:s + seg.size] = seg
     m = 1024
     r = _aamp(mp, t, m)
