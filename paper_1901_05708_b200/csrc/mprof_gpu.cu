@@ -150,7 +150,7 @@ __global__ void k_znorm_stats(const double* __restrict__ t, int L, int m, double
 // Bq[p] = 1/sqrt(S_p) (0 for a constant window) for the spread test (k_bspread).
 __global__ void k_euclid_stats(const double* __restrict__ t, int L, int m, double* __restrict__ mu,
                                double* __restrict__ S, float2* __restrict__ SB,
-                               double* __restrict__ Bq) {
+                               double* __restrict__ Bq, unsigned int* __restrict__ out_of_range) {
   const double t0 = t[0];
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -163,6 +163,8 @@ __global__ void k_euclid_stats(const double* __restrict__ t, int L, int m, doubl
     }
     mu[p] = mean0 + t0;
     S[p] = ss;
+    // the float filter tables need S and mu - t[0] well inside float range
+    if (!(ss < 1e30 && fabs(mean0) < 1e30)) atomicOr(out_of_range, 1u);
     SB[p] = make_float2(__double2float_rd(ss), __double2float_rd(mean0));
     Bq[p] = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
   }
@@ -1147,7 +1149,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     } else if (knobs().zn_filter == 2) {
       c->zn_colscale = true;
     } else {
-      if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
+      if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 3 * sizeof(double)));
       CK(cudaMemsetAsync(c->d_spread, 0, 2 * sizeof(double), c->stream));
       k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.B, L, c->d_spread);
       double h[2];
@@ -1166,19 +1168,19 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     if (ds && cfg->precision == MPROF_FP64 && knobs().aamp_cov != 0) {
       // covariance form (EuclidCov) when the window scales vary little inside the filter
       // blocks (the same spread test as the z-norm filter form; MPROF_AAMP_COV=0|1 overrides)
-      k_euclid_stats<<<g, 256, 0, c->stream>>>(d_t, L, m, w.emu, w.S, w.SB, w.cv);
-      ++*launches;
-      bool use = knobs().aamp_cov == 1;
-      if (!use) {
-        if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 2 * sizeof(double)));
-        CK(cudaMemsetAsync(c->d_spread, 0, 2 * sizeof(double), c->stream));
-        k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.cv, L, c->d_spread);
-        double h[2];
-        CK(cudaMemcpyAsync(h, c->d_spread, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        ++*launches;
-        use = h[1] > 0.0 && h[0] / h[1] >= kAampCovMinSpread;
-      }
+      if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 3 * sizeof(double)));
+      CK(cudaMemsetAsync(c->d_spread, 0, 3 * sizeof(double), c->stream));
+      unsigned int* d_oor = reinterpret_cast<unsigned int*>(c->d_spread + 2);
+      k_euclid_stats<<<g, 256, 0, c->stream>>>(d_t, L, m, w.emu, w.S, w.SB, w.cv, d_oor);
+      k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.cv, L, c->d_spread);
+      *launches += 2;
+      double h[3];
+      CK(cudaMemcpyAsync(h, c->d_spread, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      unsigned int oor;
+      std::memcpy(&oor, &h[2], sizeof oor);
+      bool use = knobs().aamp_cov == 1 || (h[1] > 0.0 && h[0] / h[1] >= kAampCovMinSpread);
+      if (oor) use = false;  // values beyond the float tables' range: (delta, sigma) kernel
       if (use) {
         k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.emu, w.A2, L, m);
         ++*launches;

@@ -85,3 +85,12 @@ def test_cov_form_bands_merge(mp):
         distances = P.cpu().numpy()
         nn_index = im.cpu().numpy()
     _parity(t, m, R)
+
+
+def test_cov_form_falls_back_beyond_float_range(mp):
+    # means beyond the float filter tables' range: the (delta, sigma) kernel runs instead
+    t = np.cumsum(np.random.default_rng(10).standard_normal(6000))
+    t[3000:] += 1e31
+    r = _aamp(mp, t, 1024)
+    assert r.info.fp64_ops_per_cell == 3.0
+    assert np.all(np.isfinite(r.distances))

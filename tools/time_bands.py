@@ -42,5 +42,34 @@ for fam, kind in engines:
             ms.append(round(best, 3))
             Rs.append(info.rows_per_tile)
         out[f"{fam}_w{world}"] = {"band_ms": ms, "max": max(ms), "sum": round(sum(ms), 3), "R": Rs}
+        # fused merge + finalize + all-gather of rank r's slice (mprof_merge_finalize_peers),
+        # with every partial local here: per-rank cost of the peer-memory merge step
+        if world > 1:
+            import time
+            from paper_1901_05708_b200.distributed import shard_range
+            parts = []
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                c_r = torch.empty(L, dtype=torch.float64, device="cuda")
+                i_r = torch.empty(L, dtype=torch.int64, device="cuda")
+                mp.sweep_device(d_t.data_ptr(), n, cfg, a, b, c_r.data_ptr(), i_r.data_ptr(), ctx=ctx)
+                parts.append((c_r, i_r))
+            outs = [(torch.empty(L, dtype=torch.float64, device="cuda"),
+                     torch.empty(L, dtype=torch.int64, device="cuda")) for _ in range(world)]
+            mms = []
+            for r in range(world):
+                lo, hi = shard_range(L, r, world)
+                best = 1e30
+                for _ in range(3):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    mp.merge_finalize_peers(d_t.data_ptr(), n, cfg, [x[0].data_ptr() for x in parts],
+                                            [x[1].data_ptr() for x in parts],
+                                            [x[0].data_ptr() for x in outs],
+                                            [x[1].data_ptr() for x in outs], lo, hi, ctx=ctx)
+                    torch.cuda.synchronize()
+                    best = min(best, (time.perf_counter() - t0) * 1e3)
+                mms.append(round(best, 3))
+            out[f"{fam}_w{world}"]["merge_finalize_ms"] = mms
+            del parts, outs
         print(fam, world, out[f"{fam}_w{world}"], flush=True)
 print(json.dumps(out))
