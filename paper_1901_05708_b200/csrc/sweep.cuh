@@ -540,7 +540,7 @@ __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhi
 // the ring (c1 = X0+s+xb, c2 = +D), the thresholds two aligned runs in the stage buffer; cell
 // (u, d) uses run entry u + d.
 template <class P, int D, bool GUARD>
-__device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0, int kt, int kend,
+__device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, int i0, int kt, int kend,
                                           int L, int rl, double p, const typename P::V2* cA1,
                                           const typename P::V2* cA2, const typename P::VB* cB1,
                                           const typename P::VB* cB2, int* cT1, int* cT2,
@@ -578,6 +578,7 @@ __device__ __noinline__ void replay_block(Acc<P, D> acc, int s, int cnt, int i0,
       if (stats) atomicAdd(&stats[1], 1ull);
     }
   }
+  return acc;  // the block's end accumulators (start of the next block of a replayed group)
 }
 
 // Merge of the seed cells (every valid cell, all lanes on the same row): columns per cell, the
@@ -619,6 +620,23 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 // row or column minimum if its key is <= theta. The hot loop keeps the running minimum key of
 // the block (a VIMNMX3 tree, no branch); a block that passes is replayed by `replay_block`.
 
+// Blocks per hit test (one data-dependent branch and one saved accumulator set per group of HG
+// blocks instead of per block; a passing group is replayed whole). Measured (sweep ms, 1 B200):
+//   covariance-only filters, HG 1 -> 2 -> 4: C4 AAMP 122.7 -> 118.4 -> 115.7, C4 ACAMP 121.7 ->
+//   116.6 -> 115.2, C5 ACAMP 2088 -> 2054 -> 2365 (C5 replays ~1e8 blocks: larger groups replay
+//   more); column-scaled z-norm (C2) 2.93 -> 2.84; p-norm p=1 (C3) 11.7 -> 12.7 (slow-settling
+//   thresholds, many replays), so value-key filters keep HG = 1. A per-block hit mask with a
+//   merge-free advance over the blocks that did not pass measured slower (C4 AAMP 117.8 at HG 4).
+#ifndef MPROF_HIT_GROUP_COV
+#define MPROF_HIT_GROUP_COV 2   // covariance-only filters (EuclidCov, Znorm)
+#endif
+#ifndef MPROF_HIT_GROUP_CS
+#define MPROF_HIT_GROUP_CS 2    // column-scaled z-norm
+#endif
+#ifndef MPROF_HIT_GROUP
+#define MPROF_HIT_GROUP 1       // value-key filters ((delta, sigma) AAMP, p-norm, FP32)
+#endif
+
 template <class P, int D, int T, int S, bool GUARD>
 __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int X0,
                                           typename P::V (&acc)[D], int i0, int cnt, int kt,
@@ -658,6 +676,8 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // the bound is kept as a raw word (hit <=> max raw(cov) >= bound), INT_MIN = every cell may
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
   constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
+  constexpr int HG = ZQ ? MPROF_HIT_GROUP_COV : (kColScale ? MPROF_HIT_GROUP_CS : MPROF_HIT_GROUP);
+  static_assert(S % (HG * D) == 0, "a full stage is whole hit groups");
   const float md_f = static_cast<float>(is_euclid_cov<P>() ? g_cell_ctx.md : 0.0);
   auto block_theta_cov = [&](int s) {
     float th;
@@ -680,67 +700,80 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   double num_nx = 0.0;
   if constexpr (ZQ) theta_nx = block_theta_cov(0);
   else block_theta(0, theta_nx, num_nx);
-  for (int s = 0; s < cnt; s += D) {
-    // the D operands entering during this block are contiguous in the ring: constant offsets
-    const int qn = G::pad((X0 + s + xb + D) % G::RING);
-    const V2* nA = &sm.colA[qn];
-    const VB* nB = &sm.colB[P::kHasB ? qn : 0];
-    const int theta = theta_nx;
-    const double num = num_nx;
-    if constexpr (ZQ) theta_nx = block_theta_cov(min(s + D, S - D));
-    else block_theta(min(s + D, S - D), theta_nx, num_nx);
+  for (int s0 = 0; s0 < cnt; s0 += HG * D) {
+    // HG blocks share one hit test (one data-dependent branch) and one saved accumulator set; a
+    // group that passes is replayed block by block from the group start.
     Acc<P, D> acc0;
 #pragma unroll
     for (int d = 0; d < D; ++d) acc0.a[d] = acc[d];
-    int hmin = ZQ ? INT_MIN : INT_MAX;  // ZQ: running MAX of raw covariance words
     bool hit = false;
 #pragma unroll
-    for (int u = 0; u < D; ++u) {
-      if (GUARD && s + u >= cnt) break;
-      const int x = s + u;
-      const V2 r = rowA[x];
-      const int row = i0 + x + 1;
-      int hu = ZQ ? INT_MIN : INT_MAX;
+    for (int g = 0; g < HG; ++g) {
+      const int s = s0 + g * D;
+      if (HG > 1 && GUARD && s >= cnt) break;
+      // the D operands entering during this block are contiguous in the ring: constant offsets
+      const int qn = G::pad((X0 + s + xb + D) % G::RING);
+      const V2* nA = &sm.colA[qn];
+      const VB* nB = &sm.colB[P::kHasB ? qn : 0];
+      const int theta = theta_nx;
+      const double num = num_nx;
+      if constexpr (ZQ) theta_nx = block_theta_cov(min(s + D, S - D));
+      else block_theta(min(s + D, S - D), theta_nx, num_nx);
+      int hmin = ZQ ? INT_MIN : INT_MAX;  // ZQ: running MAX of raw covariance words
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const int sl = (d + u) % D;
-        acc[d] = P::step(acc[d], r, cA[sl], p);
-        if constexpr (ZQ) {
-          int h = P::cov_raw(acc[d]);
-          if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MIN;
-          hu = max(hu, h);
-        } else {
-          int h;
-          if constexpr (kColScale) h = P::cov_key(acc[d] * cB[sl]);
-          else h = P::key(acc[d]);
-          if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
-          hu = min(hu, h);
+      for (int u = 0; u < D; ++u) {
+        if (GUARD && s + u >= cnt) break;
+        const int x = s + u;
+        const V2 r = rowA[x];
+        const int row = i0 + x + 1;
+        int hu = ZQ ? INT_MIN : INT_MAX;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int sl = (d + u) % D;
+          acc[d] = P::step(acc[d], r, cA[sl], p);
+          if constexpr (ZQ) {
+            int h = P::cov_raw(acc[d]);
+            if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MIN;
+            hu = max(hu, h);
+          } else {
+            int h;
+            if constexpr (kColScale) h = P::cov_key(acc[d] * cB[sl]);
+            else h = P::key(acc[d]);
+            if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MAX;
+            hu = min(hu, h);
+          }
         }
+        if constexpr (kColScale) {
+          // row bound for this sub-step: cov * B_j >= (1 - tau) / B_i
+          const int tu = (num == 0.0) ? INT_MAX
+                                      : P::cov_bound(num * static_cast<double>(sm.rowIBx[x]));
+          hit |= hu <= tu;
+        } else if constexpr (ZQ) {
+          hmin = max(hmin, hu);
+        } else {
+          hmin = min(hmin, hu);
+        }
+        // slide the column ring: slot u (used by d = 0 this substep) takes the next operand
+        cA[u] = nA[u];
+        if constexpr (kColScale) cB[u] = nB[u];
       }
-      if constexpr (kColScale) {
-        // row bound for this sub-step: cov * B_j >= (1 - tau) / B_i
-        const int tu = (num == 0.0) ? INT_MAX
-                                    : P::cov_bound(num * static_cast<double>(sm.rowIBx[x]));
-        hit |= hu <= tu;
-      } else if constexpr (ZQ) {
-        hmin = max(hmin, hu);
-      } else {
-        hmin = min(hmin, hu);
-      }
-      // slide the column ring: slot u (used by d = 0 this substep) takes the next operand
-      cA[u] = nA[u];
-      if constexpr (kColScale) cB[u] = nB[u];
+      if constexpr (ZQ) hit |= hmin >= theta;
+      else if constexpr (!kColScale) hit |= hmin <= theta;
     }
-    if constexpr (ZQ) hit = hmin >= theta;
-    else if constexpr (!kColScale) hit = hmin <= theta;
     if (hit) {
-      const int q1 = G::pad((X0 + s + xb) % G::RING);
-      const int q2 = G::pad((X0 + s + xb + D) % G::RING);
       int* colT = sm.colT[b];
-      replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, rl, p, &sm.colA[q1], &sm.colA[q2],
-                                &sm.colB[P::kHasB ? q1 : 0], &sm.colB[P::kHasB ? q2 : 0],
-                                &colT[G::pad(s + xb)], &colT[G::pad(s + xb + D)], rowA,
-                                sm.rowB[b], sm.rowT[b], best, stats);
+#pragma unroll 1
+      for (int g = 0; g < HG; ++g) {
+        const int s = s0 + g * D;
+        if (HG > 1 && GUARD && s >= cnt) break;
+        const int q1 = G::pad((X0 + s + xb) % G::RING);
+        const int q2 = G::pad((X0 + s + xb + D) % G::RING);
+        acc0 = replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, rl, p, &sm.colA[q1],
+                                         &sm.colA[q2], &sm.colB[P::kHasB ? q1 : 0],
+                                         &sm.colB[P::kHasB ? q2 : 0], &colT[G::pad(s + xb)],
+                                         &colT[G::pad(s + xb + D)], rowA, sm.rowB[b], sm.rowT[b],
+                                         best, stats);
+      }
     }
   }
 }
