@@ -399,6 +399,15 @@ struct Geo {
   static constexpr int RINGP = pad(RING - 1) + 1;
 };
 
+// Sampled keys (experiment switch, off): measured with HG = 2, sweep ms 1 B200, off -> on: C4
+// AAMP 118.4 -> 116.3, C4 ACAMP 116.4 -> 113.3, but C5 ACAMP 2056 -> 2175 and a random walk
+// n = 2^20, m = 512 ACAMP 129.0 -> 136.8: the one-step margin (m-lag differences x window
+// deviations, ~1 % of the covariance scale) is comparable to the 1 - correlation slack of the
+// nearest neighbours, so many more blocks pass and replay.
+#ifndef MPROF_SAMPLED_KEYS
+#define MPROF_SAMPLED_KEYS 0
+#endif
+
 // Shared memory of one CTA. Column operands live in a RING indexed by X = (column position -
 // tile column base): stage st uses X in [st*S, st*S + S + K) and prefetches only its S new
 // operands for stage st+1, so one copy of the K-wide window is resident (not two). Thresholds
@@ -439,6 +448,14 @@ struct SweepSmem {
   // max tau (up)} of each row block and column block pair.
   float4 erow[EQ ? S / D : 1];
   float4 ecol[EQ ? NCB : 1];
+  // Sampled keys (FP64 covariance forms): the hot loop takes the keys of sub-steps 1, 3, 5, 7
+  // only. Every other cell of the block is one slide step before a sampled cell, and one step
+  // changes a covariance by at most RX*CY + CX*RY, the per-block upper bounds {max |A.x|,
+  // max |A.y|} of the row block (drow) and the column block pair (dcol), float rounded up; the
+  // block bound is lowered by that amount.
+  static constexpr bool SK = (ZQ || EQ) && sizeof(typename P::V) == 8 && MPROF_SAMPLED_KEYS;
+  float2 drow[SK ? S / D : 1];
+  float2 dcol[SK ? NCB : 1];
 };
 
 struct SweepParams {
@@ -676,6 +693,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // the bound is kept as a raw word (hit <=> max raw(cov) >= bound), INT_MIN = every cell may
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
   constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
+  constexpr bool SKON = SweepSmem<P, D, T, S>::SK && !GUARD;  // sampled keys (interior stages)
   constexpr int HG = ZQ ? MPROF_HIT_GROUP_COV : (kColScale ? MPROF_HIT_GROUP_CS : MPROF_HIT_GROUP);
   static_assert(S % (HG * D) == 0, "a full stage is whole hit groups");
   const float md_f = static_cast<float>(is_euclid_cov<P>() ? g_cell_ctx.md : 0.0);
@@ -693,6 +711,11 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       const float2 rq = sm.zrow[s / D];
       const float2 cq = sm.zcol[s / D + threadIdx.x];
       th = fminf(__fmul_rd(rq.x, cq.y), __fmul_rd(cq.x, rq.y));
+    }
+    if constexpr (SKON) {
+      const float2 dr = sm.drow[s / D];
+      const float2 dc = sm.dcol[s / D + threadIdx.x];
+      th = __fsub_rd(th, __fmaf_ru(dr.x, dc.y, __fmul_ru(dc.x, dr.y)));
     }
     return th > 0.f ? P::cov_bound_raw_f(th) : INT_MIN;
   };
@@ -732,9 +755,11 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
           const int sl = (d + u) % D;
           acc[d] = P::step(acc[d], r, cA[sl], p);
           if constexpr (ZQ) {
-            int h = P::cov_raw(acc[d]);
-            if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MIN;
-            hu = max(hu, h);
+            if (!SKON || (u & 1)) {
+              int h = P::cov_raw(acc[d]);
+              if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) h = INT_MIN;
+              hu = max(hu, h);
+            }
           } else {
             int h;
             if constexpr (kColScale) h = P::cov_key(acc[d] * cB[sl]);
@@ -822,6 +847,50 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
   // words and takes its neighbour's from the next lane (lane 31 reduces the neighbour itself);
   // a second round covers blocks T .. NCB-1. Row blocks go to warp 1, which has no second round.
   const int t = threadIdx.x, lane = t & 31;
+  if constexpr (SM::SK) {
+    using V2 = typename P::V2;
+    // |value| upper-bound words: high word without the sign (low word taken as all ones)
+    auto absw = [](double v) { return __double2hiint(v) & 0x7FFFFFFF; };
+    auto absb = [](int w) { return __double2float_ru(__hiloint2double(w, -1)); };
+    auto dblock = [&](int blk) {
+      int2 w = make_int2(0, 0);
+      if (blk < SM::NCB) {
+        const int q = G::pad((X0 + blk * D) % G::RING);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          if (blk * D + d < G::NCOL) {
+            const V2 a = sm.colA[q + d];
+            w.x = max(w.x, absw(a.x));
+            w.y = max(w.y, absw(a.y));
+          }
+        }
+      }
+      return w;
+    };
+#pragma unroll
+    for (int base = 0; base < 2 * T; base += T) {
+      if (base >= SM::NCB - 1) break;
+      const int c = base + t;
+      const int2 v = dblock(c);
+      int2 o;
+      o.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+      o.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+      if (lane == 31) o = dblock(c + 1);
+      if (c < SM::NCB - 1) sm.dcol[c] = make_float2(absb(max(v.x, o.x)), absb(max(v.y, o.y)));
+    }
+    static_assert(S / D <= T - 64, "row blocks of the step bound on warp 2");
+    if (t >= 64 && t < 64 + S / D) {
+      const int r = t - 64;
+      int2 w = make_int2(0, 0);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const V2 a = sm.rowA[b][r * D + d];
+        w.x = max(w.x, absw(a.x));
+        w.y = max(w.y, absw(a.y));
+      }
+      sm.drow[r] = make_float2(absb(w.x), absb(w.y));
+    }
+  }
   if constexpr (SM::EQ) {
     // {min S, min mu, max mu, max tau} per aligned block of D columns; pair c = blocks c, c+1
     auto block = [&](int blk) {
