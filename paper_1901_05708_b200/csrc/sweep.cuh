@@ -641,8 +641,10 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 // blocks instead of per block; a passing group is replayed whole). Measured (sweep ms, 1 B200):
 //   covariance-only filters, HG 1 -> 2 -> 4: C4 AAMP 122.7 -> 118.4 -> 115.7, C4 ACAMP 121.7 ->
 //   116.6 -> 115.2, C5 ACAMP 2088 -> 2054 -> 2365 (C5 replays ~1e8 blocks: larger groups replay
-//   more); column-scaled z-norm (C2) 2.93 -> 2.84; p-norm p=1 (C3) 11.7 -> 12.7 (slow-settling
-//   thresholds, many replays), so value-key filters keep HG = 1. A per-block hit mask with a
+//   more); column-scaled z-norm (C2) 2.93 -> 2.84; (delta, sigma) AAMP (random walk n = 2^18,
+//   m = 128) 8.96 -> 8.83, FP32 C4 AAMP 96.5 -> 92.3; p-norm (C3) p = 1 11.7 -> 12.7, p = 3
+//   16.5 -> 17.3, p = 2.5 746 -> 776 (slow-settling thresholds, many replays), so p-norm keeps
+//   HG = 1. A per-block hit mask with a
 //   merge-free advance over the blocks that did not pass measured slower (C4 AAMP 117.8 at HG 4).
 #ifndef MPROF_HIT_GROUP_COV
 #define MPROF_HIT_GROUP_COV 2   // covariance-only filters (EuclidCov, Znorm)
@@ -650,8 +652,11 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #ifndef MPROF_HIT_GROUP_CS
 #define MPROF_HIT_GROUP_CS 2    // column-scaled z-norm
 #endif
+#ifndef MPROF_HIT_GROUP_DS
+#define MPROF_HIT_GROUP_DS 2    // (delta, sigma) AAMP, FP64 and FP32
+#endif
 #ifndef MPROF_HIT_GROUP
-#define MPROF_HIT_GROUP 1       // value-key filters ((delta, sigma) AAMP, p-norm, FP32)
+#define MPROF_HIT_GROUP 1       // other value-key filters (p-norm, exact mode)
 #endif
 
 template <class P, int D, int T, int S, bool GUARD>
@@ -694,7 +699,9 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
   constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
   constexpr bool SKON = SweepSmem<P, D, T, S>::SK && !GUARD;  // sampled keys (interior stages)
-  constexpr int HG = ZQ ? MPROF_HIT_GROUP_COV : (kColScale ? MPROF_HIT_GROUP_CS : MPROF_HIT_GROUP);
+  constexpr int HG = ZQ ? MPROF_HIT_GROUP_COV
+                       : kColScale ? MPROF_HIT_GROUP_CS
+                                   : (P::kPairs == kPairsDeltaSum ? MPROF_HIT_GROUP_DS : MPROF_HIT_GROUP);
   static_assert(S % (HG * D) == 0, "a full stage is whole hit groups");
   const float md_f = static_cast<float>(is_euclid_cov<P>() ? g_cell_ctx.md : 0.0);
   auto block_theta_cov = [&](int s) {
