@@ -652,6 +652,10 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #ifndef MPROF_HIT_GROUP_CS
 #define MPROF_HIT_GROUP_CS 2    // column-scaled z-norm
 #endif
+// Warp-uniform hit branch (experiment switch, off): C4 ACAMP 116.7 -> 119.7 ms, C5 2054 -> 2104.
+#ifndef MPROF_HIT_VOTE
+#define MPROF_HIT_VOTE 0
+#endif
 #ifndef MPROF_HIT_GROUP_DS
 #define MPROF_HIT_GROUP_DS 2    // (delta, sigma) AAMP, FP64 and FP32
 #endif
@@ -792,7 +796,13 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       if constexpr (ZQ) hit |= hmin >= theta;
       else if constexpr (!kColScale) hit |= hmin <= theta;
     }
+#if MPROF_HIT_VOTE
+    // warp-uniform branch: the whole warp replays the group when any lane passes (a lane whose
+    // group did not pass finds no cell in the replay, the filter being conservative)
+    if (__any_sync(0xffffffffu, hit)) {
+#else
     if (hit) {
+#endif
       int* colT = sm.colT[b];
 #pragma unroll 1
       for (int g = 0; g < HG; ++g) {
