@@ -124,51 +124,124 @@ __global__ void k_build_pairs(const double* __restrict__ t, double2* __restrict_
   }
 }
 
+// Window statistics, register-blocked: a CTA of kWsT threads owns kWsSpan = kWsT * kWsW
+// consecutive windows, thread tid the kWsW windows P0 + tid * kWsW + [0, kWsW). The samples are
+// staged through shared memory in chunks of kWsC window offsets (each sample read from global
+// once per CTA and chunk instead of once per window) and every thread keeps a register ring of
+// kWsW samples, so a window offset l costs ONE shared load per thread for kWsW windows. Every
+// window's sums keep the one-window loop's order l = 0..m-1, so the results are bit-identical to
+// summing each window on its own.
+#ifndef MPROF_WS_T
+#define MPROF_WS_T 128
+#endif
+constexpr int kWsW = 8, kWsT = MPROF_WS_T, kWsC = 256, kWsSpan = kWsT * kWsW;
+constexpr int kWsSmem = (kWsSpan + kWsC) + (kWsSpan + kWsC) / kWsW;  // padded: q -> q + q / kWsW
+__device__ __forceinline__ int ws_pad(int q) { return q + q / kWsW; }
+
+// One pass over the window offsets l = 0..m-1 of the CTA's windows: op(w, x) with x = sample
+// P0 + tid * kWsW + w + l (minus `shift`), in increasing l for every w.
+template <class Op>
+__device__ __forceinline__ void ws_pass(const double* __restrict__ t, int n, int P0, int m,
+                                        double shift, double* sh, Op op) {
+  const int tb = threadIdx.x * kWsW;
+  for (int l0 = 0; l0 < m; l0 += kWsC) {
+    const int cl = min(kWsC, m - l0);
+    __syncthreads();  // previous chunk / pass consumed
+    for (int q = threadIdx.x; q < kWsSpan + cl; q += kWsT) {
+      const int g = P0 + l0 + q;
+      sh[ws_pad(q)] = g < n ? t[g] - shift : 0.0;
+    }
+    __syncthreads();
+    double x[kWsW];  // slot (w + l) % kWsW holds sample tb + w + l of the chunk
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) x[w] = sh[ws_pad(tb + w)];
+    for (int lb = 0; lb < cl; lb += kWsW) {
+#pragma unroll
+      for (int u = 0; u < kWsW; ++u) {
+        const int l = lb + u;
+        if (l < cl) {
+#pragma unroll
+          for (int w = 0; w < kWsW; ++w) op(w, x[(w + u) % kWsW]);
+        }
+        const int q = tb + kWsW + l;
+        x[u] = q < kWsSpan + cl ? sh[ws_pad(q)] : 0.0;
+      }
+    }
+  }
+}
+
 // Per-window mean and inverse centred norm, two-pass (the well-conditioned form; the reference
 // derives var from running sums, acamp.hpp:42-47). Flat windows (population variance <=
 // flat_threshold, the reference's rule acamp.hpp:55-56 / oracle.cpp:81-84) get B = 0.
-__global__ void k_znorm_stats(const double* __restrict__ t, int L, int m, double flat_thr,
-                              double* __restrict__ mu, double* __restrict__ B) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int l = 0; l < m; ++l) s += t[p + l];
-    const double mean = s / m;
-    double ss = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double d = t[p + l] - mean;
-      ss = fma(d, d, ss);
+__global__ void __launch_bounds__(kWsT) k_znorm_stats(const double* __restrict__ t, int L, int m,
+                                                      double flat_thr, double* __restrict__ mu,
+                                                      double* __restrict__ B) {
+  __shared__ double sh[kWsSmem];
+  const int n = L + m - 1;
+  for (int P0 = blockIdx.x * kWsSpan; P0 < L; P0 += gridDim.x * kWsSpan) {
+    double s[kWsW], ss[kWsW], mean[kWsW];
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) s[w] = ss[w] = 0.0;
+    ws_pass(t, n, P0, m, 0.0, sh, [&](int w, double x) { s[w] += x; });
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) mean[w] = s[w] / m;
+    ws_pass(t, n, P0, m, 0.0, sh, [&](int w, double x) {
+      const double d = x - mean[w];
+      ss[w] = fma(d, d, ss[w]);
+    });
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) {
+      const int p = P0 + threadIdx.x * kWsW + w;
+      if (p < L) {
+        mu[p] = mean[w];
+        const double var = ss[w] / m;
+        B[p] = (var <= flat_thr) ? 0.0 : 1.0 / sqrt(ss[w]);
+      }
     }
-    mu[p] = mean;
-    const double var = ss / m;
-    B[p] = (var <= flat_thr) ? 0.0 : 1.0 / sqrt(ss);
   }
 }
 
 // Covariance-form AAMP statistics (EuclidCov in sweep.cuh): two-pass window mean mu_p and
 // centred sum of squares S_p (FP64, exact inputs of the comparison values), the float ring
 // scalars SB[p] = {S_p rounded down, mu_p - t[0] rounded down} of the filter tables, and
-// Bq[p] = 1/sqrt(S_p) (0 for a constant window) for the spread test (k_bspread).
-__global__ void k_euclid_stats(const double* __restrict__ t, int L, int m, double* __restrict__ mu,
-                               double* __restrict__ S, float2* __restrict__ SB,
-                               double* __restrict__ Bq, unsigned int* __restrict__ out_of_range) {
+// Bq[p] = 1/sqrt(S_p) (0 for a constant window) for the spread test (k_bspread). Same blocking
+// as k_znorm_stats; the samples are staged as t - t[0].
+__global__ void __launch_bounds__(kWsT) k_euclid_stats(const double* __restrict__ t, int L, int m,
+                                                       double* __restrict__ mu,
+                                                       double* __restrict__ S,
+                                                       float2* __restrict__ SB,
+                                                       double* __restrict__ Bq,
+                                                       unsigned int* __restrict__ out_of_range) {
+  __shared__ double sh[kWsSmem];
+  const int n = L + m - 1;
   const double t0 = t[0];
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L; p += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int l = 0; l < m; ++l) s += t[p + l] - t0;
-    const double mean0 = s / m;  // mean of t - t[0]: keeps the digits of level-offset series
-    double ss = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double d = (t[p + l] - t0) - mean0;
-      ss = fma(d, d, ss);
+  for (int P0 = blockIdx.x * kWsSpan; P0 < L; P0 += gridDim.x * kWsSpan) {
+    double s[kWsW], ss[kWsW], mean0[kWsW];
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) s[w] = ss[w] = 0.0;
+    ws_pass(t, n, P0, m, t0, sh, [&](int w, double x) { s[w] += x; });
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) mean0[w] = s[w] / m;  // mean of t - t[0]: keeps the digits of level-offset series
+    ws_pass(t, n, P0, m, t0, sh, [&](int w, double x) {
+      const double d = x - mean0[w];
+      ss[w] = fma(d, d, ss[w]);
+    });
+#pragma unroll
+    for (int w = 0; w < kWsW; ++w) {
+      const int p = P0 + threadIdx.x * kWsW + w;
+      if (p < L) {
+        mu[p] = mean0[w] + t0;
+        S[p] = ss[w];
+        // the float filter tables need S and mu - t[0] well inside float range
+        if (!(ss[w] < 1e30 && fabs(mean0[w]) < 1e30)) atomicOr(out_of_range, 1u);
+        SB[p] = make_float2(__double2float_rd(ss[w]), __double2float_rd(mean0[w]));
+        Bq[p] = ss[w] > 0.0 ? 1.0 / sqrt(ss[w]) : 0.0;
+      }
     }
-    mu[p] = mean0 + t0;
-    S[p] = ss;
-    // the float filter tables need S and mu - t[0] well inside float range
-    if (!(ss < 1e30 && fabs(mean0) < 1e30)) atomicOr(out_of_range, 1u);
-    SB[p] = make_float2(__double2float_rd(ss), __double2float_rd(mean0));
-    Bq[p] = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
   }
 }
+
+int ws_grid(int L) { return std::max(1, std::min((L + kWsSpan - 1) / kWsSpan, 148 * 8)); }
 
 // A[p] = (df_p, dg_p) for the centred-covariance slide (see Znorm in sweep.cuh).
 __global__ void k_znorm_pairs(const double* __restrict__ t, const double* __restrict__ mu,
@@ -799,7 +872,7 @@ int32_t ensure_znorm_stats(mprof_ctx* c, const double* d_t, uint64_t n, const mp
       c->stats_thr == cfg->flat_threshold)
     return MPROF_OK;
   const int L = (int)(n - cfg->m + 1);
-  k_znorm_stats<<<grid_for(L), 256, 0, c->stream>>>(d_t, L, (int)cfg->m, cfg->flat_threshold, w.mu, w.B);
+  k_znorm_stats<<<ws_grid(L), kWsT, 0, c->stream>>>(d_t, L, (int)cfg->m, cfg->flat_threshold, w.mu, w.B);
   CK(cudaGetLastError());
   c->stats_t = d_t;
   c->stats_n = n;
@@ -1171,7 +1244,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
       if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 3 * sizeof(double)));
       CK(cudaMemsetAsync(c->d_spread, 0, 3 * sizeof(double), c->stream));
       unsigned int* d_oor = reinterpret_cast<unsigned int*>(c->d_spread + 2);
-      k_euclid_stats<<<g, 256, 0, c->stream>>>(d_t, L, m, w.emu, w.S, w.SB, w.cv, d_oor);
+      k_euclid_stats<<<ws_grid(L), kWsT, 0, c->stream>>>(d_t, L, m, w.emu, w.S, w.SB, w.cv, d_oor);
       k_bspread<<<grid_for(L / (2 * kD) + 1), 256, 0, c->stream>>>(w.cv, L, c->d_spread);
       *launches += 2;
       double h[3];
