@@ -598,6 +598,81 @@ __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, in
   return acc;  // the block's end accumulators (start of the next block of a replayed group)
 }
 
+// Warp-cooperative replay of lane `src`'s hit group: lane q < D takes diagonal q of src's
+// blocks (accumulator `a` = src's acc0.a[q]), so a group replays in D sub-steps per block instead
+// of D*D cells on one lane while the other 31 lanes wait. Per sub-step every active lane
+// evaluates its cell exactly as replay_block does (same slide, same value, same clamp), offers
+// its column, and the row candidates of the D lanes are reduced lexicographically (warp
+// shuffles) into one row offer. Offers are exact lexicographic minima, so the order in which the
+// cells of a sub-step are merged does not change the result. Called convergently by the warp.
+template <class P, int D, int HG, bool GUARD>
+__device__ __noinline__ void coop_replay(typename P::V a, int src, int s0, int cnt, int i0, int kts,
+                                         int kend, int L, int rl, double p,
+                                         const typename P::V2* colA, const typename P::VB* colB,
+                                         int* colT, int X0, int xbs, int ring,
+                                         const typename P::V2* rowA, const typename P::VB* rowB,
+                                         int* rowT, BestEntry* best, unsigned long long* stats) {
+  using V2 = typename P::V2;
+  using VB = typename P::VB;
+  const int q = threadIdx.x & 31;
+  const bool act = q < D;
+  if (stats && q == 0) atomicAdd(&stats[0], 1ull);
+#pragma unroll 1
+  for (int g = 0; g < HG; ++g) {
+    const int s = s0 + g * D;
+    if (GUARD && s >= cnt) break;
+    const int q1 = (X0 + s + xbs) % ring;  // the block's two aligned runs of D ring entries
+    const int q2 = (X0 + s + xbs + D) % ring;
+#pragma unroll 1
+    for (int u = 0; u < D; ++u) {
+      if (GUARD && s + u >= cnt) break;
+      const int x = s + u;
+      const V2 r = rowA[x];
+      const VB rb = P::kHasB ? rowB[x] : VB{};
+      const int row = i0 + x + 1;
+      const int e = u + q;  // entry of the block's column run (lanes q < D)
+      const int ce = act ? (e < D ? q1 + e : q2 + e - D) : q1;
+      const V2 c = colA[ce + ce / D];
+      if (act) a = P::step(a, r, c, p);
+      const int k = kts + q;
+      const bool valid = act && (!GUARD || ((k < kend) && (row + k <= L - 1)));
+      unsigned long long rv = kInfBits;
+      int rj = INT_MAX;
+      if (valid) {
+        const int j = row + k;
+        const VB cb = P::kHasB ? colB[ce + ce / D] : VB{};
+        const double v = cell_value<P>(a, rb, cb, row, j);
+        const int h = __double2hiint(v);
+        const int xc = s + xbs + e;  // column offset within the stage window
+        int* ct = &colT[xc + xc / D];
+        const int tr = *reinterpret_cast<volatile int*>(&rowT[x]);
+        const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+        if (h <= *reinterpret_cast<volatile int*>(ct)) {
+          atomicMin(ct, static_cast<int>(offer(best, j, vb, out_index(row, rl)) >> 32));
+          if (stats) atomicAdd(&stats[1], 1ull);
+        }
+        if (h <= tr) {
+          rv = vb;
+          rj = out_index(j, rl);
+        }
+      }
+#pragma unroll
+      for (int off = D / 2; off > 0; off >>= 1) {
+        const unsigned long long ov = __shfl_xor_sync(0xffffffffu, rv, off);
+        const int oj = __shfl_xor_sync(0xffffffffu, rj, off);
+        if (lex_less(ov, oj, rv, rj)) {
+          rv = ov;
+          rj = oj;
+        }
+      }
+      if (q == 0 && rj != INT_MAX) {
+        atomicMin(&rowT[x], static_cast<int>(offer(best, row, rv, rj) >> 32));
+        if (stats) atomicAdd(&stats[1], 1ull);
+      }
+    }
+  }
+}
+
 // Merge of the seed cells (every valid cell, all lanes on the same row): columns per cell, the
 // row through a warp lexicographic reduction and one CAS per warp. Called convergently.
 template <int D>
@@ -651,6 +726,13 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #endif
 #ifndef MPROF_HIT_GROUP_CS
 #define MPROF_HIT_GROUP_CS 2    // column-scaled z-norm
+#endif
+// Warp-cooperative replay (coop_replay; experiment switch, off): parity-green, but C5 ACAMP
+// 2052 -> 2262 ms and a random walk n = 2^20, m = 512 ACAMP 129.0 -> 142.5 ms: the replays
+// cluster (several lanes of a warp pass together), and serialising them lane by lane through
+// the warp costs more than the lanes' concurrent per-lane replays.
+#ifndef MPROF_COOP_REPLAY
+#define MPROF_COOP_REPLAY 0
 #endif
 // Warp-uniform hit branch (experiment switch, off): C4 ACAMP 116.7 -> 119.7 ms, C5 2054 -> 2104.
 #ifndef MPROF_HIT_VOTE
@@ -796,6 +878,26 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
       if constexpr (ZQ) hit |= hmin >= theta;
       else if constexpr (!kColScale) hit |= hmin <= theta;
     }
+#if MPROF_COOP_REPLAY
+    if constexpr (HG > 1) {
+      unsigned pend = __ballot_sync(0xffffffffu, hit);
+      while (pend) {
+        const int src = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const int lane = threadIdx.x & 31;
+        typename P::V a{};
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const typename P::V v = __shfl_sync(0xffffffffu, acc0.a[d], src);
+          if (lane == d) a = v;
+        }
+        coop_replay<P, D, HG, GUARD>(a, src, s0, cnt, i0, kt + (src - lane) * D, kend, L, rl, p,
+                                     sm.colA, sm.colB, sm.colT[b], X0, (threadIdx.x - lane + src) * D,
+                                     G::RING, rowA, sm.rowB[b], sm.rowT[b], best, stats);
+      }
+      continue;
+    }
+#endif
 #if MPROF_HIT_VOTE
     // warp-uniform branch: the whole warp replays the group when any lane passes (a lane whose
     // group did not pass finds no cell in the replay, the filter being conservative)
