@@ -43,6 +43,43 @@ def merge_min_(cmp: torch.Tensor, idx: torch.Tensor, group=None) -> None:
     idx.copy_(torch.where(cand == INT64_MAX, torch.full_like(idx, -1), cand))
 
 
+NO_INDEX32 = 0xFFFFFFFF  # "no neighbour" in a packed key: sorts after every real index
+
+
+def pack_keys(cmp: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """FP32-mode merge keys, int64, ordered like the lexicographic (value, index) pairs of the
+    float32-rounded values: high half = the float's order-preserving integer (non-negative
+    floats keep their bits, negative ones map below them), low half = the uint32 index, "no
+    neighbour" (idx < 0) packing as NO_INDEX32. Rounding to float32 is monotone, so the order
+    is exact for the rounded values. Needs L < 2^32."""
+    bits = cmp.to(torch.float32).view(torch.int32).to(torch.int64)
+    high = torch.where(bits >= 0, bits, (~bits) - (1 << 31))
+    low = torch.where(idx >= 0, idx, torch.full_like(idx, NO_INDEX32))
+    return (high << 32) | low
+
+
+def unpack_keys(key: torch.Tensor, cmp: torch.Tensor, idx: torch.Tensor) -> None:
+    """Inverse of pack_keys into (cmp as float64 of the float32 value, idx with -1 restored)."""
+    low = key & 0xFFFFFFFF
+    idx.copy_(torch.where(low == NO_INDEX32, torch.full_like(low, -1), low))
+    high = key >> 32
+    bits = torch.where(high >= 0, high, ~(high + (1 << 31)))
+    cmp.copy_(bits.to(torch.int32).view(torch.float32).to(torch.float64))
+
+
+def merge_min_packed_(cmp: torch.Tensor, idx: torch.Tensor, group=None) -> None:
+    """FP32 mode: the merge as ONE all-reduce(MIN) over packed 64-bit (value, index) keys (the
+    north star's ncclMin on uint64 keys; 8 bytes per entry instead of two 8-byte passes). The
+    FP32 sweep's candidate values are float-valued already; the FP64 seeds round to float32 here,
+    which only reorders candidates that tie at float precision (inside FP32 mode's stated bound),
+    and finalize recomputes the reported distance of the chosen pair in FP64."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    key = pack_keys(cmp, idx)
+    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    unpack_keys(key, cmp, idx)
+
+
 def shard_size(L: int, world: int) -> int:
     return -(-L // world)
 
