@@ -218,11 +218,21 @@ struct Pnorm : KeyF64 {
 // (COLSCALE = 0: 2 DFMA per cell) or cov * B_j against a per-row bound (COLSCALE = 1:
 // + 1 DMUL per cell, tight when the window scales vary, e.g. short windows).
 template <bool COLSCALE>
+// Stage rows of the covariance-only kernels (measured, sweep ms, 128 -> 256 rows): EuclidCov C4
+// 118.4 -> 115.7, random walk n = 2^18, m = 256 8.10 -> 8.06; Znorm C4 116.6 -> 116.2 but C5
+// 2055 -> 2130 and a random walk n = 2^20, m = 512 129.1 -> 133.4, so only EuclidCov uses 256.
+#ifndef MPROF_STAGE_COV
+#define MPROF_STAGE_COV 128
+#endif
+#ifndef MPROF_STAGE_ECOV
+#define MPROF_STAGE_ECOV 256
+#endif
 struct Znorm : KeyF64 {
   using Base = Znorm;
   using V = double;
   using V2 = double2;
   using VB = double;
+  static constexpr int kStageRows = COLSCALE ? 128 : MPROF_STAGE_COV;
   static constexpr bool kHasB = true;
   static constexpr bool kCenteredSeed = true;
   static constexpr bool kCovFilter = true;
@@ -258,6 +268,7 @@ struct Znorm : KeyF64 {
 // the neighbours are within the block bound's slack. Replaces EuclidScan's slide
 // (/root/reference/proj/src/diag_scan.cpp:7-24, incremental_euclidean_step aamp.hpp:37-42).
 struct EuclidCov : KeyF64 {
+  static constexpr int kStageRows = MPROF_STAGE_ECOV;
   using Base = Euclid<false>;
   using V = double;
   using V2 = double2;
