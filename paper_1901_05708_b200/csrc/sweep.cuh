@@ -735,6 +735,12 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #ifndef MPROF_HIT_GROUP_COV
 #define MPROF_HIT_GROUP_COV 2   // covariance-only filters (EuclidCov, Znorm)
 #endif
+// covariance-form AAMP (EuclidCov), HG 2 -> 4: C4 115.7 -> 113.2, C5-shaped AAMP 1856 -> 1812, but
+// random walk m = 256 8.11 -> 8.27, C2-shaped AAMP 6.09 -> 6.48 and a sinusoid (C3 series,
+// m = 1024) 53.6 -> 74.2 (replay-heavy), so 2.
+#ifndef MPROF_HIT_GROUP_ECOV
+#define MPROF_HIT_GROUP_ECOV 2
+#endif
 #ifndef MPROF_HIT_GROUP_CS
 #define MPROF_HIT_GROUP_CS 2    // column-scaled z-norm
 #endif
@@ -796,7 +802,8 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
   constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
   constexpr bool SKON = SweepSmem<P, D, T, S>::SK && !GUARD;  // sampled keys (interior stages)
-  constexpr int HG = ZQ ? MPROF_HIT_GROUP_COV
+  constexpr int HG = SweepSmem<P, D, T, S>::EQ ? MPROF_HIT_GROUP_ECOV
+                   : ZQ ? MPROF_HIT_GROUP_COV
                        : kColScale ? MPROF_HIT_GROUP_CS
                                    : (P::kPairs == kPairsDeltaSum ? MPROF_HIT_GROUP_DS : MPROF_HIT_GROUP);
   static_assert(S % (HG * D) == 0, "a full stage is whole hit groups");
