@@ -52,6 +52,11 @@ constexpr double kZnCovFilterMinSpread = 0.955;
 // the same test for the covariance-form AAMP kernel (EuclidCov): measured on random walks,
 // m=1024 (spread 0.983) -10.7 %, m=256 (0.93) -7 %, m=128 +6.5 %, m=100 (C1) 3.9x slower
 constexpr double kAampCovMinSpread = 0.92;
+// AAMP form probe (probe_aamp_form): kProbeTiles short tiles of kProbeRows rows swept with the
+// covariance-form kernel before the main launch; above kProbeMaxReplays replayed blocks per cell
+// the (delta, sigma) kernel sweeps the band instead.
+constexpr int kProbeTiles = 148, kProbeRows = 256;
+constexpr double kProbeMaxReplays = 5e-6, kProbeMinCells = 1e10;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
@@ -760,6 +765,8 @@ struct mprof_ctx {
   bool zn_colscale = false;  // z-norm filter form chosen for the current sweep
   bool aamp_cov = false;     // AAMP form chosen for the current sweep (covariance vs delta-sigma)
   double* d_spread = nullptr;
+  int4* probe_d = nullptr;                 // AAMP form probe: tile list and replay counter
+  unsigned long long* probe_cnt = nullptr;
   mprof_progress_fn progress = nullptr;  // anytime observer (band granularity)
   void* progress_user = nullptr;
 };
@@ -1117,6 +1124,51 @@ int32_t ensure_side(mprof_ctx* c) {
 // filter on a side stream, concurrently with the rest: there correlations are ~1 and the
 // covariance-only bound (block-wide 1/B extrema) passes nearly every block, whose replays
 // would make those tiles the sweep's critical path.
+// The covariance-form AAMP filter's block bound uses block extrema of S and mu; on series whose
+// nearest-neighbour distances are small against that slack (near-periodic signals with a low
+// noise floor) most blocks pass and replay, and the (delta, sigma) kernel is several times
+// faster (C3's sinusoid at m = 1024: 53 vs 17 ms). The window-scale spread test cannot see that,
+// so the choice is confirmed on the series itself: kProbeTiles short tiles spread over the
+// band's diagonal blocks and rows are swept with the covariance kernel (after the first-diagonal
+// pass, so the thresholds are the real ones) with a replay counter. The probe cells are genuine
+// cells of the band (offers are exact minima, so sweeping them again later changes nothing).
+int32_t probe_aamp_form(mprof_ctx* c, const SweepParams& prm, int kb_lo, uint32_t* launches) {
+  const int L = prm.L, k_hi = prm.k_hi, row_hi = prm.row_hi;
+  const long long nblk = (k_hi - kb_lo + kK - 1) / kK;
+  if (nblk <= 0) return MPROF_OK;
+  std::vector<int4> pt;
+  double cells = 0.0;
+  for (int q = 0; q < kProbeTiles; ++q) {
+    const long long kb = kb_lo + kK * ((long long)q * nblk / kProbeTiles);
+    const long long rend = std::min<long long>(L - kb, row_hi);
+    if (rend <= 0) continue;
+    const long long span = std::max<long long>(1, rend - kProbeRows);
+    const long long ra = (long long)(((unsigned long long)q * 2654435761ull) % (unsigned long long)span);
+    const long long re = std::min<long long>(ra + kProbeRows, rend);
+    pt.push_back(make_int4((int)kb, (int)ra, (int)re, 0));
+    cells += (double)(re - ra) * (double)std::min<long long>(kK, k_hi - kb);
+  }
+  if (pt.empty() || cells <= 0.0) return MPROF_OK;
+  if (!c->probe_d) CK(cudaMalloc(&c->probe_d, kProbeTiles * sizeof(int4)));
+  if (!c->probe_cnt) CK(cudaMalloc(&c->probe_cnt, 2 * sizeof(unsigned long long)));
+  CK(cudaMemcpyAsync(c->probe_d, pt.data(), pt.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemsetAsync(c->probe_cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+  SweepParams pp = prm;
+  pp.tiles = c->probe_d;
+  pp.stats = c->probe_cnt;
+  int32_t st = launch_tiles<EuclidCov>(pp, 0, (long long)pt.size(), c->stream, launches);
+  if (st != MPROF_OK) return st;
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, c->probe_cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if ((double)h[0] > kProbeMaxReplays * cells) c->aamp_cov = false;
+  if (knobs().tile_debug)
+    fprintf(stderr, "[mprof probe] %zu tiles, %.3g cells, %llu replays -> %s\n", pt.size(), cells,
+            h[0], c->aamp_cov ? "covariance form" : "(delta, sigma) kernel");
+  return MPROF_OK;
+}
+
 int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
                        long long ntiles, long long n_near, int k1, bool first_diag,
                        uint32_t* launches, float* ms) {
@@ -1299,6 +1351,46 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   // would re-offer values equal to the thresholds they set (every block of those lanes replays
   // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
   const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
+  SweepParams prm;
+  prm.t = d_t;
+  prm.A = w.A;
+  prm.B = w.B;
+  prm.A32 = w.A32;
+  prm.B32 = w.B32;
+  prm.mu = c->aamp_cov && cfg->family != MPROF_ZNORMALIZED ? w.emu : w.mu;
+  prm.A2 = w.A2;
+  prm.SB = w.SB;
+  prm.S = w.S;
+  prm.best = w.best;
+  prm.tiles = nullptr;
+  prm.n = n;
+  prm.m = m;
+  prm.L = L;
+  prm.k_hi = k_hi;
+  prm.R = 0;
+  prm.row_hi = row_hi;
+  prm.rl = rl;
+  prm.p = cfg->p;
+  prm.stats = nullptr;
+  prm.scratch = w.cv;
+  // Confirm an automatically chosen covariance AAMP form on the series itself (full sweeps of
+  // large bands): the first-diagonal thresholds, then the probe, then the tiling for the kernel
+  // that will run.
+  if (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov && !cfg->exact &&
+      cfg->precision == MPROF_FP64 && knobs().aamp_cov == -1 && rl == 0 && row_hi == L &&
+      k_hi - k_tile > 2 * kK &&
+      (double)mprof_band_cells((uint64_t)n, (uint64_t)m, (uint64_t)k_tile, (uint64_t)k_hi) >= kProbeMinCells) {
+    if (first_diag) {
+      int32_t st = with_policy(c, cfg, [&]<class P>() {
+        return launch_first_diag<P>(c, prm, (int)cfg->exclusion, launches);
+      });
+      if (st != MPROF_OK) return st;
+      first_diag = false;
+    }
+    int32_t st = probe_aamp_form(c, prm, k_tile + kK, launches);
+    if (st != MPROF_OK) return st;
+    if (!c->aamp_cov) prm.mu = w.mu;
+  }
   const int S = stage_rows_for(c, cfg);
   {
     long long pbits;
@@ -1319,28 +1411,8 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   }
   int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, m, S, &out->ntiles);
   if (st != MPROF_OK) return st;
-  SweepParams prm;
-  prm.t = d_t;
-  prm.A = w.A;
-  prm.B = w.B;
-  prm.A32 = w.A32;
-  prm.B32 = w.B32;
-  prm.mu = c->aamp_cov && cfg->family != MPROF_ZNORMALIZED ? w.emu : w.mu;
-  prm.A2 = w.A2;
-  prm.SB = w.SB;
-  prm.S = w.S;
-  prm.best = w.best;
   prm.tiles = c->tiles_d;
-  prm.n = n;
-  prm.m = m;
-  prm.L = L;
-  prm.k_hi = k_hi;
   prm.R = (int)std::min<long long>(out->R, INT_MAX);
-  prm.row_hi = row_hi;
-  prm.rl = rl;
-  prm.p = cfg->p;
-  prm.stats = nullptr;
-  prm.scratch = w.cv;
   const bool want_stats = knobs().stats;
   if (want_stats) {
     CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
@@ -1589,6 +1661,8 @@ void mprof_ctx_destroy(mprof_ctx* c) {
   if (c->io) cudaFree(c->io);
   if (c->tiles_d) cudaFree(c->tiles_d);
   if (c->d_spread) cudaFree(c->d_spread);
+  if (c->probe_d) cudaFree(c->probe_d);
+  if (c->probe_cnt) cudaFree(c->probe_cnt);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->side) {
