@@ -56,7 +56,7 @@ constexpr double kAampCovMinSpread = 0.92;
 // covariance-form kernel before the main launch; above kProbeMaxReplays replayed blocks per cell
 // the (delta, sigma) kernel sweeps the band instead.
 constexpr int kProbeTiles = 148, kProbeRows = 256;
-constexpr double kProbeMaxReplays = 5e-6, kProbeMinCells = 1e10;
+constexpr double kProbeMaxReplays = 5e-6, kProbeMinCells = 4e9;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
