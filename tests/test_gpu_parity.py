@@ -427,3 +427,21 @@ def test_c5_full_acamp(mp):
     m = 512
     P, I = gpu(mp, t, m, ZNORM)
     _full_size_checks(mp, t, m, ZNORM, P, I, rows=4, pairs=10000)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("series,m,ops", [("c3", 1024, 3.0), ("c2", 256, 3.0), ("c4", 1024, 2.0)])
+def test_aamp_form_probe(mp, series, m, ops):
+    """The AAMP form probe (probe_aamp_form): on near-periodic series (the C3 sinusoids, the C2
+    motif/flat series) the covariance form's block bound passes most blocks, so the probe hands
+    the band to the (delta, sigma) kernel (3 FP64 instructions per cell in the run info); on
+    the C4 random walk it keeps the covariance form (2). Either way the profile passes the
+    full-size checks (sampled exact rows on the CPU and through the GPU brute force)."""
+    t = getattr(W, series)()
+    if series == "c4":
+        t = t[:1 << 18]
+    ts = mp.make_time_series(t)
+    r = mp.aamp(ts, mp.ProfileConfig(m, mp.DistanceKind.euclidean()))
+    assert r.info.fp64_ops_per_cell == ops
+    P, I = np.asarray(r.distances), np.asarray(r.nn_index)
+    _full_size_checks(mp, t, m, EUCLIDEAN, P, I, rows=3, pairs=5000)
