@@ -52,11 +52,16 @@ constexpr double kZnCovFilterMinSpread = 0.955;
 // the same test for the covariance-form AAMP kernel (EuclidCov): measured on random walks,
 // m=1024 (spread 0.983) -10.7 %, m=256 (0.93) -7 %, m=128 +6.5 %, m=100 (C1) 3.9x slower
 constexpr double kAampCovMinSpread = 0.92;
-// AAMP form probe (probe_aamp_form): kProbeTiles short tiles of kProbeRows rows swept with the
+// Form probe (probe_form): kProbeTiles short tiles of kProbeRows rows swept with the
 // covariance-form kernel before the main launch; above kProbeMaxReplays replayed blocks per cell
 // the (delta, sigma) kernel sweeps the band instead.
 constexpr int kProbeTiles = 148, kProbeRows = 256;
 constexpr double kProbeMaxReplays = 5e-6, kProbeMinCells = 4e9;
+// z-norm: the covariance-only filter against the column-scaled one (+1 DMUL per cell): measured
+// replayed blocks per cell of the covariance-only form where it still wins: C5 1.6e-5, random
+// walk m = 512 1.6e-5; where the column-scaled form wins: C3 sinusoids m = 1024 4.7e-5, m = 256
+// 7.1e-4.
+constexpr double kProbeMaxReplaysZ = 3e-5;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
@@ -1132,7 +1137,7 @@ int32_t ensure_side(mprof_ctx* c) {
 // band's diagonal blocks and rows are swept with the covariance kernel (after the first-diagonal
 // pass, so the thresholds are the real ones) with a replay counter. The probe cells are genuine
 // cells of the band (offers are exact minima, so sweeping them again later changes nothing).
-int32_t probe_aamp_form(mprof_ctx* c, const SweepParams& prm, int kb_lo, uint32_t* launches) {
+int32_t probe_form(mprof_ctx* c, bool zn, const SweepParams& prm, int kb_lo, uint32_t* launches) {
   const int L = prm.L, k_hi = prm.k_hi, row_hi = prm.row_hi;
   const long long nblk = (k_hi - kb_lo + kK - 1) / kK;
   if (nblk <= 0) return MPROF_OK;
@@ -1157,15 +1162,19 @@ int32_t probe_aamp_form(mprof_ctx* c, const SweepParams& prm, int kb_lo, uint32_
   SweepParams pp = prm;
   pp.tiles = c->probe_d;
   pp.stats = c->probe_cnt;
-  int32_t st = launch_tiles<EuclidCov>(pp, 0, (long long)pt.size(), c->stream, launches);
+  int32_t st = zn ? launch_tiles<Znorm<false>>(pp, 0, (long long)pt.size(), c->stream, launches)
+                  : launch_tiles<EuclidCov>(pp, 0, (long long)pt.size(), c->stream, launches);
   if (st != MPROF_OK) return st;
   unsigned long long h[2];
   CK(cudaMemcpyAsync(h, c->probe_cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if ((double)h[0] > kProbeMaxReplays * cells) c->aamp_cov = false;
+  const bool keep = (double)h[0] <= (zn ? kProbeMaxReplaysZ : kProbeMaxReplays) * cells;
+  if (zn) c->zn_colscale = !keep;
+  else c->aamp_cov = keep;
   if (knobs().tile_debug)
-    fprintf(stderr, "[mprof probe] %zu tiles, %.3g cells, %llu replays -> %s\n", pt.size(), cells,
-            h[0], c->aamp_cov ? "covariance form" : "(delta, sigma) kernel");
+    fprintf(stderr, "[mprof probe] %s: %zu tiles, %.3g cells, %llu replays -> %s\n",
+            zn ? "z-norm" : "AAMP", pt.size(), cells, h[0],
+            keep ? "covariance-only form" : zn ? "column-scaled form" : "(delta, sigma) kernel");
   return MPROF_OK;
 }
 
@@ -1373,11 +1382,13 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   prm.p = cfg->p;
   prm.stats = nullptr;
   prm.scratch = w.cv;
-  // Confirm an automatically chosen covariance AAMP form on the series itself (full sweeps of
+  // Confirm an automatically chosen covariance-only form (AAMP or z-norm) on the series itself (full sweeps of
   // large bands): the first-diagonal thresholds, then the probe, then the tiling for the kernel
   // that will run.
-  if (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov && !cfg->exact &&
-      cfg->precision == MPROF_FP64 && knobs().aamp_cov == -1 && rl == 0 && row_hi == L &&
+  const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  const bool auto_cov = zn ? (!c->zn_colscale && knobs().zn_filter == 0)
+                           : (c->aamp_cov && knobs().aamp_cov == -1);
+  if (auto_cov && !cfg->exact && cfg->precision == MPROF_FP64 && rl == 0 && row_hi == L &&
       k_hi - k_tile > 2 * kK &&
       (double)mprof_band_cells((uint64_t)n, (uint64_t)m, (uint64_t)k_tile, (uint64_t)k_hi) >= kProbeMinCells) {
     if (first_diag) {
@@ -1387,9 +1398,9 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
       if (st != MPROF_OK) return st;
       first_diag = false;
     }
-    int32_t st = probe_aamp_form(c, prm, k_tile + kK, launches);
+    int32_t st = probe_form(c, zn, prm, k_tile + kK, launches);
     if (st != MPROF_OK) return st;
-    if (!c->aamp_cov) prm.mu = w.mu;
+    if (!zn && !c->aamp_cov) prm.mu = w.mu;
   }
   const int S = stage_rows_for(c, cfg);
   {

@@ -445,3 +445,17 @@ def test_aamp_form_probe(mp, series, m, ops):
     assert r.info.fp64_ops_per_cell == ops
     P, I = np.asarray(r.distances), np.asarray(r.nn_index)
     _full_size_checks(mp, t, m, EUCLIDEAN, P, I, rows=3, pairs=5000)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("series,n,m,ops", [("c3", 262144, 1024, 3.125), ("c4", 1 << 18, 1024, 2.0)])
+def test_znorm_form_probe(mp, series, n, m, ops):
+    """The z-norm form probe: on the C3 sinusoids at m = 1024 the covariance-only filter replays
+    ~4.5e-5 blocks per cell and the probe switches the band to the column-scaled form (3.125 FP64
+    instructions per cell in the run info); on a C4 random-walk prefix it keeps the
+    covariance-only form (2). The profile passes the full-size checks either way."""
+    t = getattr(W, series)()[:n]
+    r = mp.acamp(mp.make_time_series(t), mp.ProfileConfig(m, mp.DistanceKind.znormalized()))
+    assert r.info.fp64_ops_per_cell == ops
+    P, I = np.asarray(r.distances), np.asarray(r.nn_index)
+    _full_size_checks(mp, t, m, ZNORM, P, I, rows=3, pairs=5000)
