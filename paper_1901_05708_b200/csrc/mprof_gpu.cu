@@ -62,6 +62,10 @@ constexpr double kProbeMaxReplays = 5e-6, kProbeMinCells = 4e9;
 // walk m = 512 1.6e-5; where the column-scaled form wins: C3 sinusoids m = 1024 4.7e-5, m = 256
 // 7.1e-4.
 constexpr double kProbeMaxReplaysZ = 3e-5;
+// Longer hit groups (Wide<P>) when the probe saw at most ~2 replays in its 3.9e7 cells: measured
+// HG 2 -> 4, C4 AAMP 115.7 -> 113.2 ms, C4 ACAMP 116.6 -> 115.2 ms (0 probe replays), while a
+// random walk m = 256 AAMP (10 probe replays) went 8.11 -> 8.27 and C5 (834) 2054 -> 2365.
+constexpr double kProbeWideMaxReplays = 5e-8;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
@@ -769,6 +773,7 @@ struct mprof_ctx {
   double stats_thr = -1.0;
   bool zn_colscale = false;  // z-norm filter form chosen for the current sweep
   bool aamp_cov = false;     // AAMP form chosen for the current sweep (covariance vs delta-sigma)
+  bool wide = false;         // covariance-only policy with longer hit groups (probe: no replays)
   double* d_spread = nullptr;
   int4* probe_d = nullptr;                 // AAMP form probe: tile list and replay counter
   unsigned long long* probe_cnt = nullptr;
@@ -1104,10 +1109,13 @@ int32_t with_policy(const mprof_ctx* c, const mprof_config* cfg, F&& f) {
     if (p == 4.0) return f.template operator()<PnormF32<4>>();
     return f.template operator()<PnormF32<0>>();
   }
-  if (cfg->family == MPROF_ZNORMALIZED)
-    return c->zn_colscale ? f.template operator()<Znorm<true>>() : f.template operator()<Znorm<false>>();
+  if (cfg->family == MPROF_ZNORMALIZED) {
+    if (c->zn_colscale) return f.template operator()<Znorm<true>>();
+    return c->wide ? f.template operator()<Wide<Znorm<false>>>() : f.template operator()<Znorm<false>>();
+  }
   const bool ex = cfg->exact != 0;
-  if (l2 && !ex && c->aamp_cov) return f.template operator()<EuclidCov>();
+  if (l2 && !ex && c->aamp_cov)
+    return c->wide ? f.template operator()<Wide<EuclidCov>>() : f.template operator()<EuclidCov>();
   if (l2) return ex ? f.template operator()<Euclid<true>>() : f.template operator()<Euclid<false>>();
   if (p == 1.0) return ex ? f.template operator()<Pnorm<1, true>>() : f.template operator()<Pnorm<1, false>>();
   if (p == 3.0) return ex ? f.template operator()<Pnorm<3, true>>() : f.template operator()<Pnorm<3, false>>();
@@ -1171,6 +1179,7 @@ int32_t probe_form(mprof_ctx* c, bool zn, const SweepParams& prm, int kb_lo, uin
   const bool keep = (double)h[0] <= (zn ? kProbeMaxReplaysZ : kProbeMaxReplays) * cells;
   if (zn) c->zn_colscale = !keep;
   else c->aamp_cov = keep;
+  c->wide = keep && (double)h[0] <= kProbeWideMaxReplays * cells;
   if (knobs().tile_debug)
     fprintf(stderr, "[mprof probe] %s: %zu tiles, %.3g cells, %llu replays -> %s\n",
             zn ? "z-norm" : "AAMP", pt.size(), cells, h[0],
@@ -1360,6 +1369,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   // would re-offer values equal to the thresholds they set (every block of those lanes replays
   // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
   const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
+  c->wide = false;  // set by the form probe below
   SweepParams prm;
   prm.t = d_t;
   prm.A = w.A;
@@ -1408,7 +1418,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     std::memcpy(&pbits, &cfg->p, sizeof pbits);
     const long long key[9] = {L, k_tile, k_hi, row_hi, (long long)cfg->m, cfg->exact,
                               (long long)cfg->refresh_interval,
-                              ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) | (c->aamp_cov ? 2 : 0),
+                              ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) | (c->aamp_cov ? 2 : 0) | (c->wide ? 4 : 0),
                               pbits};
     if (std::equal(key, key + 9, c->R_key)) {
       out->R = c->R_val;

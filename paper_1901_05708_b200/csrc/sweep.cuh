@@ -296,6 +296,23 @@ struct EuclidCov : KeyF64 {
   }
 };
 
+// A covariance-only policy with longer hit groups, selected per series by the form probe when
+// its sample saw (almost) no replays: a group of HG_WIDE blocks per data-dependent branch (the
+// replay of a passing group costs more, so replay-heavy series keep the policy's own HG).
+#ifndef MPROF_HIT_GROUP_WIDE
+#define MPROF_HIT_GROUP_WIDE 4
+#endif
+template <class P>
+struct Wide : P {
+  static constexpr int kHitGroup = MPROF_HIT_GROUP_WIDE;
+};
+
+template <class P>
+constexpr int hit_group_of() {
+  if constexpr (requires { P::kHitGroup; }) return P::kHitGroup;
+  else return 0;
+}
+
 template <class P>
 constexpr bool is_euclid_cov() {
   if constexpr (requires { P::kEuclidCov; }) return P::kEuclidCov;
@@ -802,7 +819,8 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
   constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
   constexpr bool SKON = SweepSmem<P, D, T, S>::SK && !GUARD;  // sampled keys (interior stages)
-  constexpr int HG = SweepSmem<P, D, T, S>::EQ ? MPROF_HIT_GROUP_ECOV
+  constexpr int HG = hit_group_of<P>() ? hit_group_of<P>()
+                   : SweepSmem<P, D, T, S>::EQ ? MPROF_HIT_GROUP_ECOV
                    : ZQ ? MPROF_HIT_GROUP_COV
                        : kColScale ? MPROF_HIT_GROUP_CS
                                    : (P::kPairs == kPairsDeltaSum ? MPROF_HIT_GROUP_DS : MPROF_HIT_GROUP);
