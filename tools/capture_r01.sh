@@ -9,4 +9,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-fi
 python tools/time_c4.py C4aamp > /dev/null && ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:sweep_kernel<mpg::Wide<mpg::EuclidCov' -c 1 -o gpurun_out/aamp python tools/time_c4.py C4aamp > gpurun_out/ncu_a.log 2>&1
 python tools/time_c4.py C4acamp > /dev/null && ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:sweep_kernel<mpg::Wide<mpg::Znorm<\(bool\)0>' -c 1 -o gpurun_out/acamp python tools/time_c4.py C4acamp > gpurun_out/ncu_z.log 2>&1
 python tools/time_c4.py C4aamp C4acamp C5 C2 C3p1 C3p3 C1 > gpurun_out/time_c4.json 2>&1
+# summarise on the box (two --set full reports exceed gpurun's 64 MiB copy-back limit)
+python tools/ncu_summary.py $TAG --launches gpurun_out/launches.csv --rep gpurun_out/aamp.ncu-rep --rep gpurun_out/acamp.ncu-rep > gpurun_out/summary.log 2>&1
+cp profiles/${TAG}_* profiles/ncu_summary.json gpurun_out/
+rm -f gpurun_out/acamp.ncu-rep
 ls -la gpurun_out
