@@ -299,8 +299,10 @@ struct EuclidCov : KeyF64 {
 // A covariance-only policy with longer hit groups, selected per series by the form probe when
 // its sample saw (almost) no replays: a group of HG_WIDE blocks per data-dependent branch (the
 // replay of a passing group costs more, so replay-heavy series keep the policy's own HG).
+// (measured with the probe gating, sweep ms HG 4 -> 8 -> 16: C4 AAMP 112.9 -> 109.9 -> 140.5,
+// C4 ACAMP 114.5 -> 112.3 -> 129.0; 16 spills)
 #ifndef MPROF_HIT_GROUP_WIDE
-#define MPROF_HIT_GROUP_WIDE 4
+#define MPROF_HIT_GROUP_WIDE 8
 #endif
 template <class P>
 struct Wide : P {
