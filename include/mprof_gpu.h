@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MPROF_GPU_ABI_VERSION 1
+#define MPROF_GPU_ABI_VERSION 2
 
 /* Status codes. 1..13 are mprof::ErrorCode + 1 in declaration order
  * (/root/reference/proj/include/mprof/core.hpp:16-30); >= 100 are device-side failures. */
@@ -94,6 +94,15 @@ typedef struct mprof_run_info {
   float sweep_ms;            /* CUDA-event time of the sweep kernel alone (0 if not timed) */
   float fp64_ops_per_cell;   /* FP64-pipe instructions the sweep kernel issues per cell */
   float fp32_ops_per_cell;   /* FP32 instructions per cell (FP32 mode) */
+  /* the sweep kernel's policy ("Wide<EuclidCov>", "Znorm<0>", "Euclid", "Pnorm<3>", ...; the
+   * diagonal block next to the exclusion zone of a covariance-form sweep runs "Euclid" /
+   * "Znorm<1>" on a side stream) and its blocks per hit test */
+  char policy[32];
+  int32_t hit_group;
+  /* form probe (covariance-form sweeps of >= 4e9 cells): replayed blocks / cells of its sample;
+   * 0 / 0 when no probe ran */
+  uint32_t probe_replays;
+  uint64_t probe_cells;
 } mprof_run_info;
 
 typedef struct mprof_ctx mprof_ctx;
@@ -129,6 +138,14 @@ int32_t mprof_ctx_set_timing(mprof_ctx* ctx, int32_t enabled);
  * profile holds the exact minimum over the completed diagonals. NULL disables (one launch). */
 typedef int32_t (*mprof_progress_fn)(uint64_t done, uint64_t total, void* user);
 int32_t mprof_ctx_set_progress(mprof_ctx* ctx, mprof_progress_fn fn, void* user);
+/* Filter form of the FP64 fast-mode Euclidean and z-normalized sweeps. AUTO (default): chosen per
+ * series (window-scale spread test + form probe). COV: covariance-only filter (EuclidCov /
+ * Znorm<0>) with its own hit groups; WIDE: the same with the long hit groups (Wide<...>);
+ * ALT: the (delta, sigma) Euclidean kernel / the column-scaled z-norm filter. Every form gives
+ * the exact minimum under the same parity rules; this selects which kernel decides it (tests,
+ * experiments). p-norm, exact and FP32 sweeps ignore it. */
+enum { MPROF_FORM_AUTO = 0, MPROF_FORM_COV = 1, MPROF_FORM_WIDE = 2, MPROF_FORM_ALT = 3 };
+int32_t mprof_ctx_set_form(mprof_ctx* ctx, int32_t form);
 
 /* ---- reference entry points (host buffers) ------------------------------------------------ */
 /* P[L] and I[L], L = n - m + 1, caller-allocated. `threads` (reference: CPU workers) selects
@@ -232,6 +249,16 @@ uint64_t mprof_state_series_length(const mprof_state* st);
 int32_t mprof_state_profile(mprof_state* st, double* P, int64_t* I, double* cmp);
 /* The state's series (n samples) to a host buffer. */
 int32_t mprof_state_series(const mprof_state* st, double* t);
+/* Diagonals the build completed, ascending from exclusion (EngineState::completed_diagonals,
+ * /root/reference/proj/include/mprof/engine_state.hpp:33): n - m - exclusion + 1 for a complete
+ * state; fewer when the build's progress observer cancelled. mprof_state_extend refuses an
+ * incomplete state with MPROF_E_INCOMPLETE_STATE (src/engine_state.cpp:56-58). */
+uint64_t mprof_state_completed_diagonals(const mprof_state* st);
+/* Tail state of every completed diagonal k = exclusion + r at its last cell (pos = n - m - k),
+ * evaluated directly on the GPU (EngineState::tail_cursors / znorm_cursors, engine_state.hpp:
+ * 34-35): Euclidean / p-norm acc[r] = the comparison-space accumulator; z-normalized
+ * acc[5r .. 5r+4] = (sum_left, sum_right, sumsq_left, sumsq_right, dot). */
+int32_t mprof_state_tail(const mprof_state* st, double* acc);
 void mprof_state_destroy(mprof_state* st);
 
 /* ---- one process, several GPUs ------------------------------------------------------------ */

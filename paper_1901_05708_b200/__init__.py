@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = [
     "ErrorCode", "Error", "DistanceFamily", "DistanceKind", "DiagonalOrder", "AcampVariant",
-    "Precision", "ProfileConfig", "TimeSeries", "make_time_series", "validate_config",
+    "Precision", "Form", "ProfileConfig", "TimeSeries", "make_time_series", "validate_config",
     "profile_length", "default_flat_threshold", "MatrixProfile", "RunInfo", "aamp",
     "aamp_pnorm", "acamp", "sweep_device", "finalize_device", "merge_device", "band_cuts",
     "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context", "EngineState",
@@ -110,6 +110,14 @@ class AcampVariant(enum.IntEnum):
 class Precision(enum.IntEnum):
     FP64 = 0
     FP32 = 1
+
+
+class Form(enum.IntEnum):
+    """Filter form override (MPROF_FORM_*): which kernel decides a fast-mode FP64 sweep."""
+    Auto = 0
+    Cov = 1     # EuclidCov / Znorm<0>
+    Wide = 2    # Wide<EuclidCov> / Wide<Znorm<0>>
+    Alt = 3     # Euclid (delta, sigma) / Znorm<1> (column-scaled)
 
 
 def default_flat_threshold(m: int) -> float:
@@ -212,10 +220,19 @@ class RunInfo(C.Structure):
     _fields_ = [("cells", C.c_uint64), ("diagonals", C.c_uint64), ("tiles", C.c_uint64),
                 ("rows_per_tile", C.c_uint64), ("kernel_launches", C.c_uint32),
                 ("sweep_ms", C.c_float), ("fp64_ops_per_cell", C.c_float),
-                ("fp32_ops_per_cell", C.c_float)]
+                ("fp32_ops_per_cell", C.c_float), ("_policy", C.c_char * 32),
+                ("hit_group", C.c_int32), ("probe_replays", C.c_uint32),
+                ("probe_cells", C.c_uint64)]
+
+    @property
+    def policy(self) -> str:
+        """The sweep kernel's policy, e.g. "Wide<EuclidCov>", "Znorm<0>", "Pnorm<3>"."""
+        return self._policy.decode()
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
+        d["policy"] = self.policy
+        return d
 
 
 EXPORTS = {
@@ -258,7 +275,10 @@ EXPORTS = {
     "mprof_state_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mprof_state_series": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "mprof_state_destroy": (None, [C.c_void_p]),
+    "mprof_state_completed_diagonals": (C.c_uint64, [C.c_void_p]),
+    "mprof_state_tail": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "mprof_ctx_set_progress": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mprof_ctx_set_form": (C.c_int32, [C.c_void_p, C.c_int32]),
     "mprof_brute_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
                                         C.c_void_p, C.c_void_p]),
     "mprof_brute_rows": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
@@ -353,6 +373,10 @@ class Context:
 
     def set_timing(self, on: bool) -> None:
         _raise(lib().mprof_ctx_set_timing(self.handle, 1 if on else 0))
+
+    def set_form(self, form: "Form") -> None:
+        """Filter form of FP64 fast-mode Euclidean / z-norm sweeps (mprof_ctx_set_form)."""
+        _raise(lib().mprof_ctx_set_form(self.handle, int(form)))
 
     def close(self) -> None:
         if self.handle:
@@ -597,9 +621,27 @@ class EngineState:
     def comparison(self) -> np.ndarray:
         return self._load()[2]
 
+    @property
+    def completed_diagonals(self) -> np.ndarray:
+        """Ascending offsets k of the diagonals the build completed (engine_state.hpp:33)."""
+        done = int(lib().mprof_state_completed_diagonals(self._h))
+        return np.arange(self.cfg.exclusion, self.cfg.exclusion + done, dtype=np.int64)
+
+    def tail(self) -> np.ndarray:
+        """Tail accumulators per completed diagonal (mprof_state_tail): shape (done,) or
+        (done, 5) for z-normalized states (the five DiagStats sums)."""
+        done = int(lib().mprof_state_completed_diagonals(self._h))
+        five = self.cfg.kind.family == DistanceFamily.ZNormalized
+        out = np.empty((done, 5) if five else done)
+        _raise(lib().mprof_state_tail(self._h, out.ctypes.data))
+        return out
+
     def complete(self) -> bool:
-        # the GPU sweep cannot be cancelled mid-way: every diagonal always completes
-        return True
+        """True when every diagonal of the build ran (engine_state.hpp:37-39); a build cancelled
+        by its progress observer is incomplete and extend_profile refuses it."""
+        n = int(lib().mprof_state_series_length(self._h))
+        total = n - self.cfg.m - self.cfg.exclusion + 1
+        return int(lib().mprof_state_completed_diagonals(self._h)) == total
 
 
 def build_engine_state(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Callable] = None,
@@ -610,10 +652,17 @@ def build_engine_state(ts: TimeSeries, cfg: ProfileConfig, progress: Optional[Ca
     h = C.c_void_p()
     info = RunInfo()
     c = _to_c(cfg)
-    _raise(lib().mprof_state_build(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
-                                   C.byref(h), C.byref(info)))
+    cb = None
     if progress is not None:
-        progress(int(info.diagonals), int(info.diagonals))
+        # anytime observer: band-granular chunks; False cancels -> an incomplete state
+        cb = PROGRESS_FN(lambda done, total, _u: 1 if progress(int(done), int(total)) else 0)
+        _raise(lib().mprof_ctx_set_progress(_ctx_handle(ctx), C.cast(cb, C.c_void_p), None))
+    try:
+        _raise(lib().mprof_state_build(_ctx_handle(ctx), v.ctypes.data, v.shape[0], C.byref(c),
+                                       C.byref(h), C.byref(info)))
+    finally:
+        if cb is not None:
+            lib().mprof_ctx_set_progress(_ctx_handle(ctx), None, None)
     return EngineState(h, cfg.copy(), info)
 
 
@@ -621,6 +670,10 @@ def extend_profile(state: EngineState, new_samples: Sequence[float]) -> EngineSt
     """engine_state.hpp:52: a NEW state for the extended series (the input is unchanged).
     NonFinite for a bad sample; an empty span returns an equal state."""
     s = np.ascontiguousarray(np.asarray(new_samples, dtype=np.float64).reshape(-1))
+    if not state.complete():  # engine_state.cpp:56-58: before the sample checks
+        done = int(lib().mprof_state_completed_diagonals(state._h))
+        raise Error(ErrorCode.IncompleteState,
+                    f"cannot extend a partially computed profile ({done} diagonals done)")
     bad = np.flatnonzero(~np.isfinite(s))
     if bad.size:
         raise Error(ErrorCode.NonFinite, f"appended sample {int(bad[0])} is not finite")

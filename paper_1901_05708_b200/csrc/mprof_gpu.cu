@@ -563,6 +563,46 @@ __global__ void k_unreverse(const BestEntry* __restrict__ in, BestEntry* __restr
     out[i] = in[L - 1 - i];
 }
 
+// EngineState tail cursors: for completed diagonal k = excl + r, the window pair (pos, pos + k)
+// at its last cell (pos = L - 1 - k, partner L - 1), evaluated directly by one warp:
+// Euclidean / p-norm: the comparison-space accumulator (DiagonalCursor::acc, aamp.hpp:27-32);
+// z-normalized: the five sums of DiagStats (acamp.hpp:12-20) into out[5r .. 5r+4].
+__global__ void k_tail(const double* __restrict__ t, int L, int m, int excl, int count, int family,
+                       double p, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < count; r += warps) {
+    const int k = excl + r, i = L - 1 - k, j = L - 1;
+    double a = 0.0, b = 0.0, aa = 0.0, bb = 0.0, ab = 0.0;
+    for (int l = lane; l < m; l += 32) {
+      const double x = t[i + l], y = t[j + l];
+      if (family == MPROF_ZNORMALIZED) {
+        a += x; b += y; aa = fma(x, x, aa); bb = fma(y, y, bb); ab = fma(x, y, ab);
+      } else if (family == MPROF_EUCLIDEAN || p == 2.0) {
+        a = fma(x - y, x - y, a);
+      } else {
+        const double d = fabs(x - y);
+        a += p == 1.0 ? d : p == 3.0 ? d * d * d : p == 4.0 ? (d * d) * (d * d) : pow(d, p);
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+      aa += __shfl_xor_sync(0xffffffffu, aa, off);
+      bb += __shfl_xor_sync(0xffffffffu, bb, off);
+      ab += __shfl_xor_sync(0xffffffffu, ab, off);
+    }
+    if (lane == 0) {
+      if (family == MPROF_ZNORMALIZED) {
+        double* o = out + 5LL * r;
+        o[0] = a; o[1] = b; o[2] = aa; o[3] = bb; o[4] = ab;
+      } else {
+        out[r] = a;
+      }
+    }
+  }
+}
+
 // An empty partial profile (a band without diagonals): +inf / no neighbour.
 __global__ void k_split_empty(double* __restrict__ cmp, int64_t* __restrict__ idx, int L) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
@@ -779,11 +819,14 @@ struct mprof_ctx {
   unsigned long long* probe_cnt = nullptr;
   mprof_progress_fn progress = nullptr;  // anytime observer (band granularity)
   void* progress_user = nullptr;
+  int form = MPROF_FORM_AUTO;             // filter-form override (mprof_ctx_set_form)
+  unsigned long long probe_replays = 0;   // last form probe: replayed blocks / sample cells
+  double probe_cells = 0.0;
 };
 
 // Device-resident EngineState: the series, the comparison-space profile and scratch.
 struct mprof_state {
-  mprof_ctx* ctx = nullptr;
+  mprof_ctx* ctx = nullptr;  // owned: the state's own stream and workspace (any thread may use it)
   mprof_config cfg;
   uint64_t n = 0;
   double* t = nullptr;       // series (device)
@@ -798,6 +841,7 @@ struct mprof_state {
   size_t fwd_bytes = 0;
   double* P = nullptr;       // finalized distances scratch [L]
   size_t P_bytes = 0;
+  uint64_t done = 0;         // completed diagonals, ascending from cfg.exclusion (build may cancel)
 };
 
 namespace {
@@ -812,7 +856,13 @@ int32_t ensure(void** p, size_t* have, size_t need) {
   return MPROF_OK;
 }
 
-thread_local std::unordered_map<int, mprof_ctx*> g_default_ctx;
+// Default contexts (ctx == NULL): one per device and calling thread, destroyed when the thread
+// exits, so a thread pool does not leak workspaces and no two threads share a workspace.
+struct DefaultContexts {
+  std::unordered_map<int, mprof_ctx*> by_device;
+  ~DefaultContexts();
+};
+thread_local DefaultContexts g_default_ctx;
 
 int32_t resolve_ctx(mprof_ctx* in, mprof_ctx** out) {
   if (in) {
@@ -822,20 +872,52 @@ int32_t resolve_ctx(mprof_ctx* in, mprof_ctx** out) {
   }
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  auto it = g_default_ctx.find(dev);
-  if (it != g_default_ctx.end()) {
+  auto it = g_default_ctx.by_device.find(dev);
+  if (it != g_default_ctx.by_device.end()) {
     *out = it->second;
     return MPROF_OK;
   }
   mprof_ctx* c = nullptr;
   const int32_t st = mprof_ctx_create(dev, &c);
   if (st != MPROF_OK) return st;
-  g_default_ctx[dev] = c;
+  g_default_ctx.by_device[dev] = c;
   *out = c;
   return MPROF_OK;
 }
 
+DefaultContexts::~DefaultContexts() {
+  // mprof_ctx_destroy erases its entry: take the contexts out first
+  std::vector<mprof_ctx*> cs;
+  for (auto& kv : by_device) cs.push_back(kv.second);
+  by_device.clear();
+  for (mprof_ctx* c : cs) mprof_ctx_destroy(c);
+}
+
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// A state's own context: same device and form override as the context it derives from.
+int32_t state_ctx(const mprof_ctx* from, mprof_ctx** out) {
+  const int32_t st = mprof_ctx_create(from->device, out);
+  if (st != MPROF_OK) return st;
+  (*out)->form = from->form;
+  return MPROF_OK;
+}
+
+// Releases a context's transient device memory (states keep only series + profile between calls).
+void trim_ctx(mprof_ctx* c) {
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->ws);
+  cudaFree(c->io);
+  cudaFree(c->tiles_d);
+  c->ws = c->io = nullptr;
+  c->tiles_d = nullptr;
+  c->ws_bytes = c->io_bytes = c->tiles_cap = 0;
+  std::fill(c->tiles_key, c->tiles_key + 8, -1LL);
+  c->stats_t = nullptr;
+}
+
+// Diagonals of a complete state: [exclusion, n - m] (engine_state.hpp:37-39).
+uint64_t state_total(const mprof_state* S) { return S->n - S->cfg.m - S->cfg.exclusion + 1; }
 
 struct Workspace {
   double2* A;
@@ -1176,6 +1258,8 @@ int32_t probe_form(mprof_ctx* c, bool zn, const SweepParams& prm, int kb_lo, uin
   unsigned long long h[2];
   CK(cudaMemcpyAsync(h, c->probe_cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  c->probe_replays = h[0];
+  c->probe_cells = cells;
   const bool keep = (double)h[0] <= (zn ? kProbeMaxReplaysZ : kProbeMaxReplays) * cells;
   if (zn) c->zn_colscale = !keep;
   else c->aamp_cov = keep;
@@ -1286,8 +1370,13 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     if (st != MPROF_OK) return st;
     k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.mu, w.A, L, m);
     *launches += 2;
-    // filter form for this series (MPROF_ZN_FILTER=cov|col overrides the measured choice)
-    if (knobs().zn_filter == 1) {
+    // filter form for this series (mprof_ctx_set_form, then MPROF_ZN_FILTER=cov|col, override
+    // the measured choice)
+    if (c->form == MPROF_FORM_COV || c->form == MPROF_FORM_WIDE) {
+      c->zn_colscale = false;
+    } else if (c->form == MPROF_FORM_ALT) {
+      c->zn_colscale = true;
+    } else if (knobs().zn_filter == 1) {
       c->zn_colscale = false;
     } else if (knobs().zn_filter == 2) {
       c->zn_colscale = true;
@@ -1308,7 +1397,9 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     k_build_pairs<<<g, 256, 0, c->stream>>>(d_t, w.A, L, m, ds ? kPairsDeltaSum : kPairsRaw);
     ++*launches;
     c->aamp_cov = false;
-    if (ds && cfg->precision == MPROF_FP64 && knobs().aamp_cov != 0) {
+    const bool forced = c->form != MPROF_FORM_AUTO;
+    if (ds && cfg->precision == MPROF_FP64 && c->form != MPROF_FORM_ALT &&
+        (forced || knobs().aamp_cov != 0)) {
       // covariance form (EuclidCov) when the window scales vary little inside the filter
       // blocks (the same spread test as the z-norm filter form; MPROF_AAMP_COV=0|1 overrides)
       if (!c->d_spread) CK(cudaMalloc(&c->d_spread, 3 * sizeof(double)));
@@ -1322,7 +1413,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
       CK(cudaStreamSynchronize(c->stream));
       unsigned int oor;
       std::memcpy(&oor, &h[2], sizeof oor);
-      bool use = knobs().aamp_cov == 1 || (h[1] > 0.0 && h[0] / h[1] >= kAampCovMinSpread);
+      bool use = forced || knobs().aamp_cov == 1 || (h[1] > 0.0 && h[0] / h[1] >= kAampCovMinSpread);
       if (oor) use = false;  // values beyond the float tables' range: (delta, sigma) kernel
       if (use) {
         k_znorm_pairs<<<g, 256, 0, c->stream>>>(d_t, w.emu, w.A2, L, m);
@@ -1369,7 +1460,9 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   // would re-offer values equal to the thresholds they set (every block of those lanes replays
   // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
   const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
-  c->wide = false;  // set by the form probe below
+  c->wide = c->form == MPROF_FORM_WIDE;  // else set by the form probe below
+  c->probe_replays = 0;
+  c->probe_cells = 0.0;
   SweepParams prm;
   prm.t = d_t;
   prm.A = w.A;
@@ -1396,8 +1489,9 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   // large bands): the first-diagonal thresholds, then the probe, then the tiling for the kernel
   // that will run.
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
-  const bool auto_cov = zn ? (!c->zn_colscale && knobs().zn_filter == 0)
-                           : (c->aamp_cov && knobs().aamp_cov == -1);
+  const bool auto_cov = c->form == MPROF_FORM_AUTO &&
+                        (zn ? (!c->zn_colscale && knobs().zn_filter == 0)
+                            : (c->aamp_cov && knobs().aamp_cov == -1));
   if (auto_cov && !cfg->exact && cfg->precision == MPROF_FP64 && rl == 0 && row_hi == L &&
       k_hi - k_tile > 2 * kK &&
       (double)mprof_band_cells((uint64_t)n, (uint64_t)m, (uint64_t)k_tile, (uint64_t)k_hi) >= kProbeMinCells) {
@@ -1494,6 +1588,14 @@ void fill_info(mprof_ctx* c, const mprof_config* cfg, uint64_t cells, long long 
   info->rows_per_tile = (uint64_t)so.R;
   info->kernel_launches = launches;
   info->sweep_ms = so.ms;
+  std::memset(info->policy, 0, sizeof info->policy);
+  with_policy(c, cfg, [&]<class P>() {
+    std::snprintf(info->policy, sizeof info->policy, "%s", policy_name<P>());
+    info->hit_group = hit_group_for<P>();
+    return 0;
+  });
+  info->probe_replays = (uint32_t)std::min<unsigned long long>(c->probe_replays, UINT32_MAX);
+  info->probe_cells = (uint64_t)c->probe_cells;
 }
 
 int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_config* cfg,
@@ -1693,8 +1795,8 @@ void mprof_ctx_destroy(mprof_ctx* c) {
     cudaEventDestroy(c->ev_join);
   }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
-  for (auto it = g_default_ctx.begin(); it != g_default_ctx.end(); ++it)
-    if (it->second == c) { g_default_ctx.erase(it); break; }
+  for (auto it = g_default_ctx.by_device.begin(); it != g_default_ctx.by_device.end(); ++it)
+    if (it->second == c) { g_default_ctx.by_device.erase(it); break; }
   delete c;
 }
 
@@ -2101,9 +2203,16 @@ int32_t mprof_state_build(mprof_ctx* in, const double* t, uint64_t n, const mpro
   if (st != MPROF_OK) return st;
   st = check_config(n, cfg);
   if (st != MPROF_OK) return st;
-  mprof_ctx* c = nullptr;
-  st = resolve_ctx(in, &c);
+  mprof_ctx* caller = nullptr;
+  st = resolve_ctx(in, &caller);
   if (st != MPROF_OK) return st;
+  // the state owns its context (stream + workspace): it may be extended or cloned from any thread
+  // while the caller's context is in use elsewhere, and it outlives the caller's thread
+  mprof_ctx* c = nullptr;
+  st = state_ctx(caller, &c);
+  if (st != MPROF_OK) return st;
+  c->progress = caller->progress;  // a cancelled build leaves an incomplete state
+  c->progress_user = caller->progress_user;
   mprof_state* S = new mprof_state();
   S->ctx = c;
   S->cfg = *cfg;
@@ -2115,8 +2224,13 @@ int32_t mprof_state_build(mprof_ctx* in, const double* t, uint64_t n, const mpro
   if (st != MPROF_OK) { mprof_state_destroy(S); return st; }
   cudaError_t e = cudaMemcpyAsync(S->t, t, n * sizeof(double), cudaMemcpyHostToDevice, c->stream);
   if (e != cudaSuccess) { mprof_state_destroy(S); return cuda_fail(e, "cudaMemcpyAsync"); }
-  st = sweep_impl(c, S->t, n, cfg, 0, 0, S->cmp, S->idx, info);
+  mprof_run_info local{};
+  st = sweep_impl(c, S->t, n, cfg, 0, 0, S->cmp, S->idx, info ? info : &local);
+  c->progress = nullptr;
+  c->progress_user = nullptr;
   if (st != MPROF_OK) { mprof_state_destroy(S); return st; }
+  S->done = (info ? info : &local)->diagonals;
+  trim_ctx(c);
   *out = S;
   return MPROF_OK;
 }
@@ -2124,6 +2238,10 @@ int32_t mprof_state_build(mprof_ctx* in, const double* t, uint64_t n, const mpro
 int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count,
                            mprof_run_info* info) {
   if (!S) return fail(MPROF_E_BAD_ARG, "null state");
+  if (S->done != state_total(S))  // engine_state.cpp:56-58: checked before anything else
+    return fail(MPROF_E_INCOMPLETE_STATE,
+                "cannot extend a partially computed profile (%llu of %llu diagonals done)",
+                (unsigned long long)S->done, (unsigned long long)state_total(S));
   if (count == 0) {
     if (info) std::memset(info, 0, sizeof *info);
     return MPROF_OK;  // extend_profile with an empty span returns the state unchanged
@@ -2191,6 +2309,8 @@ int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count
   ++launches;
   CK(cudaGetLastError());
   S->n = n_new;
+  S->done = state_total(S);
+  trim_ctx(c);
   // cells swept: diagonals k in [excl, L_new) contribute min(dL, L_new - k)
   uint64_t cells = 0;
   for (long long k = k_lo; k < L_new; ++k) cells += (uint64_t)std::min<long long>(dL, L_new - k);
@@ -2200,12 +2320,15 @@ int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count
 
 int32_t mprof_state_clone(const mprof_state* S, mprof_state** out) {
   if (!S || !out) return fail(MPROF_E_BAD_ARG, "null argument");
-  mprof_ctx* c = S->ctx;
-  CK(cudaSetDevice(c->device));
+  mprof_ctx* c = nullptr;
+  int32_t st0 = state_ctx(S->ctx, &c);
+  if (st0 != MPROF_OK) return st0;
+  CK(cudaStreamSynchronize(S->ctx->stream));  // S's pending work (build / extend) is complete
   mprof_state* R = new mprof_state();
   R->ctx = c;
   R->cfg = S->cfg;
   R->n = S->n;
+  R->done = S->done;
   const uint64_t L = S->n - S->cfg.m + 1;
   int32_t st = ensure(reinterpret_cast<void**>(&R->t), &R->t_bytes, S->n * sizeof(double));
   if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&R->cmp), &R->cmp_bytes, L * sizeof(double));
@@ -2237,6 +2360,7 @@ int32_t mprof_state_profile(mprof_state* S, double* P, int64_t* I, double* cmp) 
   if (I) CK(cudaMemcpyAsync(I, S->idx, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   if (cmp) CK(cudaMemcpyAsync(cmp, S->cmp, L * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  trim_ctx(c);
   return MPROF_OK;
 }
 
@@ -2258,7 +2382,30 @@ void mprof_state_destroy(mprof_state* S) {
   cudaFree(S->rev);
   cudaFree(S->fwd);
   cudaFree(S->P);
+  mprof_ctx_destroy(S->ctx);
   delete S;
+}
+
+uint64_t mprof_state_completed_diagonals(const mprof_state* S) { return S ? S->done : 0; }
+
+int32_t mprof_state_tail(const mprof_state* S, double* acc) {
+  if (!S || !acc) return fail(MPROF_E_BAD_ARG, "null argument");
+  if (S->done == 0) return MPROF_OK;
+  mprof_ctx* c = S->ctx;
+  CK(cudaSetDevice(c->device));
+  const int sums = S->cfg.family == MPROF_ZNORMALIZED ? 5 : 1;
+  const size_t bytes = (size_t)S->done * sums * sizeof(double);
+  double* d = nullptr;
+  CK(cudaMallocAsync(&d, bytes, c->stream));
+  k_tail<<<grid_for(32LL * (long long)S->done), 256, 0, c->stream>>>(
+      S->t, (int)(S->n - S->cfg.m + 1), (int)S->cfg.m, (int)S->cfg.exclusion, (int)S->done,
+      S->cfg.family, S->cfg.p, d);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(acc, d, bytes, cudaMemcpyDeviceToHost, c->stream);
+  cudaFreeAsync(d, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mprof_state_tail");
+  return MPROF_OK;
 }
 
 int32_t mprof_ctx_set_progress(mprof_ctx* in, mprof_progress_fn fn, void* user) {
@@ -2267,6 +2414,16 @@ int32_t mprof_ctx_set_progress(mprof_ctx* in, mprof_progress_fn fn, void* user) 
   if (st != MPROF_OK) return st;
   c->progress = fn;
   c->progress_user = user;
+  return MPROF_OK;
+}
+
+int32_t mprof_ctx_set_form(mprof_ctx* in, int32_t form) {
+  if (form < MPROF_FORM_AUTO || form > MPROF_FORM_ALT) return fail(MPROF_E_BAD_ARG, "unknown form %d", form);
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  c->form = form;
+  c->R_key[0] = -1;  // the rows-per-tile cache is keyed on the form flags, not the override
   return MPROF_OK;
 }
 

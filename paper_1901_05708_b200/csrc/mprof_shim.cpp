@@ -2,6 +2,7 @@
 // Replaces the reference's src/aamp.cpp, src/acamp.cpp, src/core.cpp, src/oracle.cpp
 // (brute_profile) and src/engine_state.cpp for a GPU build: same validation order and error
 // codes, MatrixProfile returned by value.
+#include <algorithm>
 #include <cmath>
 #include <string>
 
@@ -113,6 +114,103 @@ MatrixProfile acamp(const TimeSeries& ts, const ProfileConfig& cfg, AcampVariant
   });
 }
 
+// ---- host-side primitives of the public API ---------------------------------------------------
+// The reference's direct (non-incremental) evaluations and the throwing five-sum helpers
+// (/root/reference/proj/src/oracle.cpp:51-93, src/acamp.cpp:9-27). They are O(m) per call, exist
+// for callers that cross-check engines, and are not on the sweep path; the summation order is the
+// reference's (l = 0..m-1, no contraction), so their results match it bit for bit.
+
+namespace {
+
+void require_window(const TimeSeries& ts, std::size_t at, std::size_t m, const char* which) {
+  if (m == 0 || at + m > ts.size())
+    throw Error(ErrorCode::OutOfRange, std::string(which) + " window of length " + std::to_string(m) +
+                                           " at " + std::to_string(at) + " does not fit " +
+                                           std::to_string(ts.size()) + " samples");
+}
+
+// Population mean and variance from plain sums (oracle.cpp:35-47), variance floored at 0.
+void window_moments(const TimeSeries& ts, std::size_t at, std::size_t m, double* mean, double* var) {
+  double s = 0.0, s2 = 0.0;
+  for (std::size_t l = 0; l < m; ++l) {
+    const double x = ts[at + l];
+    s += x;
+    s2 += x * x;
+  }
+  const double md = static_cast<double>(m);
+  *mean = s / md;
+  double v = s2 / md - *mean * *mean;
+  if (v < 0.0) v = 0.0;
+  *var = v;
+}
+
+}  // namespace
+
+DiagStats init_diag_stats(const TimeSeries& ts, std::size_t k, std::size_t m) {
+  if (m == 0 || k + m > ts.size())
+    throw Error(ErrorCode::OutOfRange, "window pair (0, " + std::to_string(k) + ") of length " +
+                                           std::to_string(m) + " does not fit " +
+                                           std::to_string(ts.size()) + " samples");
+  DiagStats s;
+  s.offset = k;
+  s.pos = 0;
+  for (std::size_t l = 0; l < m; ++l) {
+    const double a = ts[l], b = ts[k + l];
+    s.sum_left += a;
+    s.sum_right += b;
+    s.sumsq_left += a * a;
+    s.sumsq_right += b * b;
+    s.dot += a * b;
+  }
+  return s;
+}
+
+double f_score(const DiagStats& s, std::size_t m, double flat_threshold) {
+  const double md = static_cast<double>(m);
+  const double scaled_flat = flat_threshold * md;
+  if (detail::scaled_var_left(s, md) <= scaled_flat || detail::scaled_var_right(s, md) <= scaled_flat)
+    throw Error(ErrorCode::Degenerate, "f_score is undefined for a flat window (flat-window convention applies)");
+  return detail::f_value(s, md, scaled_flat);
+}
+
+double dist_euclidean(const TimeSeries& ts, std::size_t i, std::size_t j, std::size_t m) {
+  require_window(ts, i, m, "left");
+  require_window(ts, j, m, "right");
+  double acc = 0.0;
+  for (std::size_t l = 0; l < m; ++l) {
+    const double d = ts[i + l] - ts[j + l];
+    acc += d * d;
+  }
+  return std::sqrt(acc);
+}
+
+double dist_pnorm(const TimeSeries& ts, std::size_t i, std::size_t j, std::size_t m, double p) {
+  require_window(ts, i, m, "left");
+  require_window(ts, j, m, "right");
+  if (!(p >= 1.0)) throw Error(ErrorCode::BadP, "p-norm exponent must be >= 1, got " + std::to_string(p));
+  double acc = 0.0;
+  for (std::size_t l = 0; l < m; ++l) acc += detail::abs_pow(ts[i + l] - ts[j + l], p);
+  return std::pow(acc, 1.0 / p);
+}
+
+double dist_znorm(const TimeSeries& ts, std::size_t i, std::size_t j, std::size_t m,
+                  double flat_threshold) {
+  require_window(ts, i, m, "left");
+  require_window(ts, j, m, "right");
+  double mi, vi, mj, vj;
+  window_moments(ts, i, m, &mi, &vi);
+  window_moments(ts, j, m, &mj, &vj);
+  const bool fi = vi <= flat_threshold, fj = vj <= flat_threshold;
+  if (fi || fj) return (fi && fj) ? 0.0 : std::sqrt(2.0 * static_cast<double>(m));
+  const double si = 1.0 / std::sqrt(vi), sj = 1.0 / std::sqrt(vj);
+  double acc = 0.0;
+  for (std::size_t l = 0; l < m; ++l) {
+    const double d = (ts[i + l] - mi) * si - (ts[j + l] - mj) * sj;
+    acc += d * d;
+  }
+  return std::sqrt(acc);
+}
+
 MatrixProfile brute_profile(const TimeSeries& ts, const ProfileConfig& cfg) {
   return run(ts, cfg, {}, [&](const mprof_config* c, double* P, int64_t* I, mprof_run_info*) {
     return mprof_brute_profile(nullptr, ts.data(), ts.size(), c, P, I);
@@ -145,7 +243,33 @@ EngineState snapshot(std::shared_ptr<mprof_state> dev, const ProfileConfig& cfg)
   mp.nn_index = std::move(I);
   mp.m = cfg.m;
   mp.kind = cfg.kind;
-  return EngineState{make_time_series(std::move(t)), cfg, std::move(mp), std::move(cmp), std::move(dev)};
+  // completed diagonals (ascending from the exclusion) and their tail cursors
+  const uint64_t done = mprof_state_completed_diagonals(dev.get());
+  const bool zn = cfg.kind.family == DistanceFamily::ZNormalized;
+  std::vector<double> tail(done * (zn ? 5 : 1));
+  if (done) {
+    st = mprof_state_tail(dev.get(), tail.data());
+    if (st != MPROF_OK) rethrow(st);
+  }
+  std::vector<std::size_t> diags(done);
+  std::vector<DiagonalCursor> pc;
+  std::vector<ZnormCursor> zc;
+  (zn ? zc.reserve(done) : pc.reserve(done));
+  for (uint64_t r = 0; r < done; ++r) {
+    const std::size_t k = cfg.exclusion + r;
+    diags[r] = k;
+    const std::size_t pos = n - cfg.m - k;  // the diagonal's last cell
+    if (zn) {
+      ZnormCursor z;
+      z.stats = DiagStats{tail[5 * r], tail[5 * r + 1], tail[5 * r + 2], tail[5 * r + 3],
+                          tail[5 * r + 4], k, pos};
+      zc.push_back(z);
+    } else {
+      pc.push_back(DiagonalCursor{k, pos, tail[r], 0});
+    }
+  }
+  return EngineState{make_time_series(std::move(t)), cfg,        std::move(mp), std::move(cmp),
+                     std::move(diags),                std::move(pc), std::move(zc), std::move(dev)};
 }
 
 }  // namespace
@@ -156,7 +280,7 @@ EngineState build_engine_state(const TimeSeries& ts, const ProfileConfig& cfg, P
   mprof_state* raw = nullptr;
   int32_t st;
   {
-    ProgressScope scope(progress);
+    ProgressScope scope(progress);  // the observer may cancel: the state is then incomplete
     st = mprof_state_build(nullptr, ts.data(), ts.size(), &c, &raw, nullptr);
   }
   if (st != MPROF_OK) rethrow(st);
@@ -164,6 +288,12 @@ EngineState build_engine_state(const TimeSeries& ts, const ProfileConfig& cfg, P
 }
 
 EngineState extend_profile(const EngineState& state, std::span<const double> new_samples) {
+  // engine_state.cpp:56-66 order: IncompleteState, then the empty span, then NonFinite
+  if (!state.complete())
+    throw Error(ErrorCode::IncompleteState,
+                "cannot extend a partially computed profile (" +
+                    std::to_string(state.completed_diagonals.size()) + " diagonals done)");
+  if (new_samples.empty()) return state;
   for (std::size_t i = 0; i < new_samples.size(); ++i)
     if (!std::isfinite(new_samples[i]))
       throw Error(ErrorCode::NonFinite, "appended sample " + std::to_string(i) + " is not finite");

@@ -26,6 +26,7 @@
 
 #include <cstdint>
 #include <climits>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace mpg {
@@ -47,19 +48,29 @@ __device__ __forceinline__ bool lex_less(unsigned long long v, long long i, unsi
 
 // Exact lexicographic min-update of best[pos] with (v, idx); returns the resulting value bits.
 // MinBuffer::update (/root/reference/proj/src/detail/diag_scan.hpp:37-43) as a lock-free
-// 128-bit CAS loop. The initial 16-byte read may be torn by a concurrent CAS; the CAS then
-// fails and returns the true entry.
+// 128-bit CAS loop. The initial 16-byte read is not guaranteed single-copy atomic: a torn read
+// that makes the entry look smaller than it is (e.g. the new value with the old, smaller index)
+// would drop a valid offer. So a "no improvement" verdict is only returned after an atomic
+// snapshot (a CAS that writes back what it compares with) confirmed the entry it was based on;
+// an improving offer is decided by its own CAS.
 __device__ __forceinline__ unsigned long long offer(BestEntry* best, long long pos,
                                                     unsigned long long v, long long idx) {
   const longlong2 raw = __ldcg(reinterpret_cast<const longlong2*>(best + pos));
   BestEntry cur{static_cast<unsigned long long>(raw.x), raw.y};
-  while (lex_less(v, idx, cur.v, cur.idx)) {
-    const BestEntry nv{v, idx};
-    const BestEntry old = atomicCAS(best + pos, cur, nv);
-    if (old.v == cur.v && old.idx == cur.idx) return v;
-    cur = old;
+  bool atomic_read = false;  // cur was returned by a CAS (an atomic read of the entry)
+  for (;;) {
+    if (lex_less(v, idx, cur.v, cur.idx)) {
+      const BestEntry old = atomicCAS(best + pos, cur, BestEntry{v, idx});
+      if (old.v == cur.v && old.idx == cur.idx) return v;
+      cur = old;
+    } else {
+      if (atomic_read) return cur.v;
+      const BestEntry snap = atomicCAS(best + pos, cur, cur);
+      if (snap.v == cur.v && snap.idx == cur.idx) return cur.v;
+      cur = snap;
+    }
+    atomic_read = true;
   }
-  return cur.v;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -415,6 +426,34 @@ struct ZnormF32 : KeyF32 {
     return fma(a, b - mub, acc);
   }
 };
+
+// Name of a sweep policy as reported in mprof_run_info::policy.
+template <class P>
+constexpr const char* policy_name() {
+  if constexpr (std::is_same_v<P, Euclid<false>>) return "Euclid";
+  else if constexpr (std::is_same_v<P, Euclid<true>>) return "Euclid<exact>";
+  else if constexpr (std::is_same_v<P, EuclidCov>) return "EuclidCov";
+  else if constexpr (std::is_same_v<P, Wide<EuclidCov>>) return "Wide<EuclidCov>";
+  else if constexpr (std::is_same_v<P, Znorm<false>>) return "Znorm<0>";
+  else if constexpr (std::is_same_v<P, Znorm<true>>) return "Znorm<1>";
+  else if constexpr (std::is_same_v<P, Wide<Znorm<false>>>) return "Wide<Znorm<0>>";
+  else if constexpr (std::is_same_v<P, Pnorm<1, false>>) return "Pnorm<1>";
+  else if constexpr (std::is_same_v<P, Pnorm<3, false>>) return "Pnorm<3>";
+  else if constexpr (std::is_same_v<P, Pnorm<4, false>>) return "Pnorm<4>";
+  else if constexpr (std::is_same_v<P, Pnorm<0, false>>) return "Pnorm<p>";
+  else if constexpr (std::is_same_v<P, Pnorm<1, true>>) return "Pnorm<1,exact>";
+  else if constexpr (std::is_same_v<P, Pnorm<3, true>>) return "Pnorm<3,exact>";
+  else if constexpr (std::is_same_v<P, Pnorm<4, true>>) return "Pnorm<4,exact>";
+  else if constexpr (std::is_same_v<P, Pnorm<0, true>>) return "Pnorm<p,exact>";
+  else if constexpr (std::is_same_v<P, EuclidF32>) return "EuclidF32";
+  else if constexpr (std::is_same_v<P, PnormF32<1>>) return "PnormF32<1>";
+  else if constexpr (std::is_same_v<P, PnormF32<3>>) return "PnormF32<3>";
+  else if constexpr (std::is_same_v<P, PnormF32<4>>) return "PnormF32<4>";
+  else if constexpr (std::is_same_v<P, PnormF32<0>>) return "PnormF32<p>";
+  else if constexpr (std::is_same_v<P, ZnormF32<false>>) return "ZnormF32<0>";
+  else if constexpr (std::is_same_v<P, ZnormF32<true>>) return "ZnormF32<1>";
+  else return "?";
+}
 
 // ---------------------------------------------------------------------------------------------
 // Tile geometry and shared memory.
@@ -781,6 +820,18 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #define MPROF_HIT_GROUP 1       // other value-key filters (p-norm, exact mode)
 #endif
 
+// Blocks per hit test of policy P's kernel (the policy's own choice, else per filter kind).
+template <class P>
+__host__ __device__ constexpr int hit_group_for() {
+  constexpr bool EQ = is_euclid_cov<P>();
+  constexpr bool ZQ = P::kCovFilter && !P::kColScale && !EQ;
+  if constexpr (hit_group_of<P>() != 0) return hit_group_of<P>();
+  else if constexpr (EQ) return MPROF_HIT_GROUP_ECOV;
+  else if constexpr (ZQ) return MPROF_HIT_GROUP_COV;
+  else if constexpr (P::kColScale) return MPROF_HIT_GROUP_CS;
+  else return P::kPairs == kPairsDeltaSum ? MPROF_HIT_GROUP_DS : MPROF_HIT_GROUP;
+}
+
 template <class P, int D, int T, int S, bool GUARD>
 __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int X0,
                                           typename P::V (&acc)[D], int i0, int cnt, int kt,
@@ -821,11 +872,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
   // pass. Computed unconditionally (index clamped) so it schedules into the block's FP64 work.
   constexpr bool ZQ = SweepSmem<P, D, T, S>::ZQ || SweepSmem<P, D, T, S>::EQ;  // raw cov keys
   constexpr bool SKON = SweepSmem<P, D, T, S>::SK && !GUARD;  // sampled keys (interior stages)
-  constexpr int HG = hit_group_of<P>() ? hit_group_of<P>()
-                   : SweepSmem<P, D, T, S>::EQ ? MPROF_HIT_GROUP_ECOV
-                   : ZQ ? MPROF_HIT_GROUP_COV
-                       : kColScale ? MPROF_HIT_GROUP_CS
-                                   : (P::kPairs == kPairsDeltaSum ? MPROF_HIT_GROUP_DS : MPROF_HIT_GROUP);
+  constexpr int HG = hit_group_for<P>();
   static_assert(S % (HG * D) == 0, "a full stage is whole hit groups");
   const float md_f = static_cast<float>(is_euclid_cov<P>() ? g_cell_ctx.md : 0.0);
   auto block_theta_cov = [&](int s) {
