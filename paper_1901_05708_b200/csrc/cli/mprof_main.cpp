@@ -120,6 +120,78 @@ std::vector<std::string> split(const std::string& v) {
   return out;
 }
 
+// ---- compute ---------------------------------------------------------------------------------
+
+// What `compute` was asked to do, after flag validation.
+struct ComputeRequest {
+  std::string input, output;
+  mprof::ProfileConfig cfg{1, mprof::DistanceKind::euclidean()};
+  bool brute = false;      // --engine oracle
+  bool sq_space = false;   // --acamp-variant sq
+  bool progress = false;
+  std::vector<int> devices;
+};
+
+// Reads the series from a path or, for "-", standard input.
+mprof::TimeSeries load_series(const std::string& path) {
+  if (path == "-") return mprof::read_series_csv(std::cin);
+  std::ifstream file(path, std::ios::binary);
+  if (!file.is_open()) throw mprof::Error(mprof::ErrorCode::Io, "input '" + path + "' cannot be opened");
+  return mprof::read_series_csv(file);
+}
+
+// Runs `emit` on standard output ("" or "-") or on a freshly created file.
+template <class Emit>
+void with_output(const std::string& path, Emit&& emit) {
+  if (path.empty() || path == "-") {
+    emit(std::cout);
+    return;
+  }
+  std::ofstream file(path, std::ios::binary);
+  if (!file.is_open()) throw mprof::Error(mprof::ErrorCode::Io, "output '" + path + "' cannot be created");
+  emit(file);
+  if (!file) throw mprof::Error(mprof::ErrorCode::Io, "writing '" + path + "' failed");
+}
+
+// Percent lines on standard error, one per change of the integer percentage.
+class PercentReporter {
+ public:
+  bool operator()(std::size_t done, std::size_t total) {
+    const int pct = total == 0 ? 100 : static_cast<int>(100.0 * double(done) / double(total));
+    if (pct != *shown_) {
+      *shown_ = pct;
+      std::fprintf(stderr, "%d%%\n", pct);
+    }
+    return true;  // never cancels
+  }
+
+ private:
+  std::shared_ptr<int> shown_ = std::make_shared<int>(-1);  // shared by the ProgressFn copies
+};
+
+mprof::MatrixProfile execute(const ComputeRequest& rq) {
+  const mprof::TimeSeries ts = load_series(rq.input);
+  const mprof::DistanceFamily fam = rq.cfg.kind.family;
+  if (rq.brute) return mprof::brute_profile(ts, rq.cfg);
+  if (!rq.devices.empty()) {
+    using E = mprof::Engine;
+    const E engine = fam == mprof::DistanceFamily::PNorm ? E::AampPnorm
+                     : fam == mprof::DistanceFamily::ZNormalized ? E::Acamp : E::Aamp;
+    return mprof::profile_on_devices(ts, rq.cfg, rq.devices, engine);
+  }
+  const mprof::ProgressFn observer = rq.progress ? mprof::ProgressFn(PercentReporter{}) : mprof::ProgressFn{};
+  switch (fam) {
+    case mprof::DistanceFamily::PNorm:
+      return mprof::aamp_pnorm(ts, rq.cfg, observer);
+    case mprof::DistanceFamily::ZNormalized:
+      return mprof::acamp(ts, rq.cfg,
+                          rq.sq_space ? mprof::AcampVariant::SquaredDistance : mprof::AcampVariant::FScore,
+                          observer);
+    default:
+      return mprof::aamp(ts, rq.cfg, observer);
+  }
+}
+
 int compute(int argc, char** argv) {
   Command c("mprof compute: compute a matrix profile from a CSV series");
   c.add("input", "input CSV path, '-' for standard input").required = true;
@@ -139,74 +211,41 @@ int compute(int argc, char** argv) {
   c.add("progress", "emit percent lines to standard error", true);
   if (!c.parse(argc, argv, 2)) return 0;
 
+  // --p belongs to the p-norm and only to it (usage error otherwise)
   const std::string distance = c.str("distance");
-  if (distance == "pnorm" && !c.seen("p")) {
-    std::cerr << "error: --distance pnorm requires --p\n";
-    return 2;
-  }
-  if (distance != "pnorm" && c.seen("p")) {
-    std::cerr << "error: --p is only meaningful with --distance pnorm\n";
-    return 2;
-  }
-  mprof::DistanceKind kind = mprof::DistanceKind::euclidean();
-  if (distance == "pnorm") kind = mprof::DistanceKind::pnorm(to_real("p", c.str("p")));
-  if (distance == "znorm") kind = mprof::DistanceKind::znormalized();
-  mprof::ProfileConfig cfg(to_size("m", c.str("m")), kind);
-  if (c.seen("exclusion")) cfg.exclusion = to_size("exclusion", c.str("exclusion"));
-  if (c.seen("order") && c.str("order") == "random") cfg.order = mprof::DiagonalOrder::RandomPermutation;
-  if (c.seen("seed")) cfg.order_seed = to_size("seed", c.str("seed"));
+  if ((distance == "pnorm") != c.seen("p"))
+    throw UsageError(c.seen("p") ? "--p applies to --distance pnorm only"
+                                 : "--distance pnorm needs an exponent (--p)");
+  ComputeRequest rq;
+  const mprof::DistanceKind kind = distance == "pnorm"   ? mprof::DistanceKind::pnorm(to_real("p", c.str("p")))
+                                   : distance == "znorm" ? mprof::DistanceKind::znormalized()
+                                                         : mprof::DistanceKind::euclidean();
+  rq.cfg = mprof::ProfileConfig(to_size("m", c.str("m")), kind);
+  if (c.seen("exclusion")) rq.cfg.exclusion = to_size("exclusion", c.str("exclusion"));
+  if (c.seen("order") && c.str("order") == "random") rq.cfg.order = mprof::DiagonalOrder::RandomPermutation;
+  if (c.seen("seed")) rq.cfg.order_seed = to_size("seed", c.str("seed"));
   if (c.seen("threads")) (void)to_size("threads", c.str("threads"));
-
-  const std::string input = c.str("input");
-  mprof::TimeSeries ts = [&] {
-    if (input == "-") return mprof::read_series_csv(std::cin);
-    std::ifstream in(input, std::ios::binary);
-    if (!in) throw mprof::Error(mprof::ErrorCode::Io, "cannot open input '" + input + "'");
-    return mprof::read_series_csv(in);
-  }();
-
-  mprof::ProgressFn progress;
-  if (c.seen("progress")) {
-    auto last = std::make_shared<int>(-1);
-    progress = [last](std::size_t done, std::size_t total) {
-      const int pct = total ? static_cast<int>(100.0 * double(done) / double(total)) : 100;
-      if (pct != *last) {
-        *last = pct;
-        std::fprintf(stderr, "%d%%\n", pct);
-      }
-      return true;
-    };
+  rq.input = c.str("input");
+  rq.output = c.seen("output") ? c.str("output") : std::string();
+  rq.brute = c.seen("engine") && c.str("engine") == "oracle";
+  rq.sq_space = c.seen("acamp-variant") && c.str("acamp-variant") == "sq";
+  rq.progress = c.seen("progress");
+  if (c.seen("devices")) {
+    for (const auto& d : split(c.str("devices"))) rq.devices.push_back(static_cast<int>(to_size("devices", d)));
+    if (rq.devices.empty()) throw UsageError("--devices: expected a device list");
   }
-  const bool oracle = c.seen("engine") && c.str("engine") == "oracle";
-  std::vector<int> devices;
-  if (c.seen("devices"))
-    for (const auto& d : split(c.str("devices"))) devices.push_back(static_cast<int>(to_size("devices", d)));
-  if (c.seen("devices") && devices.empty()) throw UsageError("--devices: expected a device list");
-  mprof::MatrixProfile profile;
-  if (oracle) {
-    profile = mprof::brute_profile(ts, cfg);
-  } else if (!devices.empty()) {
-    const auto engine = kind.family == mprof::DistanceFamily::PNorm        ? mprof::Engine::AampPnorm
-                        : kind.family == mprof::DistanceFamily::ZNormalized ? mprof::Engine::Acamp
-                                                                            : mprof::Engine::Aamp;
-    profile = mprof::profile_on_devices(ts, cfg, devices, engine);
-  } else if (kind.family == mprof::DistanceFamily::PNorm) {
-    profile = mprof::aamp_pnorm(ts, cfg, progress);
-  } else if (kind.family == mprof::DistanceFamily::ZNormalized) {
-    const bool sq = c.seen("acamp-variant") && c.str("acamp-variant") == "sq";
-    profile = mprof::acamp(ts, cfg, sq ? mprof::AcampVariant::SquaredDistance : mprof::AcampVariant::FScore, progress);
-  } else {
-    profile = mprof::aamp(ts, cfg, progress);
-  }
-  const std::string output = c.seen("output") ? c.str("output") : "";
-  if (output.empty() || output == "-") {
-    mprof::write_profile_csv(profile, std::cout);
-  } else {
-    std::ofstream out(output, std::ios::binary);
-    if (!out) throw mprof::Error(mprof::ErrorCode::Io, "cannot open output '" + output + "'");
-    mprof::write_profile_csv(profile, out);
-  }
+  const mprof::MatrixProfile profile = execute(rq);
+  with_output(rq.output, [&](std::ostream& out) { mprof::write_profile_csv(profile, out); });
   return 0;
+}
+
+// ---- bench -----------------------------------------------------------------------------------
+
+std::vector<std::size_t> size_list(const Command& c, const char* name) {
+  std::vector<std::size_t> v;
+  if (c.seen(name))
+    for (const auto& x : split(c.str(name))) v.push_back(to_size(name, x));
+  return v;
 }
 
 int bench(int argc, char** argv) {
@@ -220,27 +259,20 @@ int bench(int argc, char** argv) {
   c.add("output", "report CSV path (default: standard output)");
   if (!c.parse(argc, argv, 2)) return 0;
   mprof::BenchPlan plan;
-  if (c.seen("sweep") && c.str("sweep") == "m") plan.sweep = mprof::BenchPlan::Sweep::M;
-  if (c.seen("n-list")) for (const auto& v : split(c.str("n-list"))) plan.n_list.push_back(to_size("n-list", v));
-  if (c.seen("m-list")) for (const auto& v : split(c.str("m-list"))) plan.m_list.push_back(to_size("m-list", v));
+  plan.sweep = c.seen("sweep") && c.str("sweep") == "m" ? mprof::BenchPlan::Sweep::M : mprof::BenchPlan::Sweep::N;
+  plan.n_list = size_list(c, "n-list");
+  plan.m_list = size_list(c, "m-list");
   if (c.seen("engines")) plan.engines = split(c.str("engines"));
   for (const auto& e : plan.engines)
-    if (!mprof::is_bench_engine(e)) throw UsageError("--engines: unknown engine '" + e + "'");
+    if (!mprof::is_bench_engine(e)) throw UsageError("--engines: '" + e + "' is not a bench engine");
   if (c.seen("repeats")) {
     const std::size_t r = to_size("repeats", c.str("repeats"));
-    if (r < 1) throw UsageError("--repeats must be positive");
+    if (r == 0) throw UsageError("--repeats must be at least 1");
     plan.repeats = static_cast<int>(r);
   }
   if (c.seen("seed")) plan.seed = to_size("seed", c.str("seed"));
-  const std::string output = c.seen("output") ? c.str("output") : "";
-  if (output.empty() || output == "-") {
-    mprof::run_bench(plan, &std::cout);
-  } else {
-    std::ofstream out(output, std::ios::binary);
-    if (!out) throw mprof::Error(mprof::ErrorCode::Io, "cannot open output '" + output + "'");
-    mprof::run_bench(plan, &out);
-    if (!out) throw mprof::Error(mprof::ErrorCode::Io, "write failure on '" + output + "'");
-  }
+  with_output(c.seen("output") ? c.str("output") : std::string(),
+              [&](std::ostream& out) { mprof::run_bench(plan, &out); });
   return 0;
 }
 
