@@ -362,7 +362,7 @@ __global__ void k_first_diag(SweepParams prm, int k1) {
           (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
       prm.scratch[i] = __longlong_as_double(static_cast<long long>(vb));
       const BestEntry cur = prm.best[i];
-      const long long jo = out_index(j, prm.rl);
+      const long long jo = j;
       if (lex_less(vb, jo, cur.v, cur.idx)) prm.best[i] = BestEntry{vb, jo};
     }
   }
@@ -375,7 +375,7 @@ __global__ void k_first_diag_cols(SweepParams prm, int k1) {
     const int j = i + k1;
     const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(prm.scratch[i]));
     const BestEntry cur = prm.best[j];
-    const long long io = out_index(i, prm.rl);
+    const long long io = i;
     if (lex_less(vb, io, cur.v, cur.idx)) prm.best[j] = BestEntry{vb, io};
   }
 }
@@ -533,34 +533,18 @@ __global__ void k_brute(const double* __restrict__ t, int L, int m, int excl, in
 }
 
 // ---- streaming extension (build_engine_state / extend_profile) -----------------------------
-__global__ void k_reverse(const double* __restrict__ in, double* __restrict__ out, int n) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    out[p] = in[n - 1 - p];
-}
-
-// Profile of the reversed extended series before the sweep of the new cells: reversed position
-// x' holds original window L_new-1-x'. The dL new windows (x' < dL) start empty; old windows
-// carry their (comparison value, original index) entry; flat windows are pinned (k_init_best).
-__global__ void k_init_from_prev(BestEntry* __restrict__ best, const double* __restrict__ B,
-                                 const double* __restrict__ cmp_old,
-                                 const int64_t* __restrict__ idx_old, int L_old, int L_new) {
-  const int dL = L_new - L_old;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < L_new; x += gridDim.x * blockDim.x) {
-    BestEntry e{kInfBits, kNoIdx};
-    if (B && B[x] == 0.0) {
-      e = BestEntry{0ull, -1};
-    } else if (x >= dL) {
-      const int o = L_new - 1 - x;
-      const long long j = idx_old[o];
-      if (j >= 0) e = BestEntry{static_cast<unsigned long long>(__double_as_longlong(cmp_old[o])), j};
-    }
-    best[x] = e;
+// The stored profile of the first l_old windows seeds the extended sweep: entry i takes the
+// lexicographic minimum with its stored (comparison value, neighbour); pinned flat windows (B = 0)
+// keep their pin (k_flat_fix sets them at the end), untouched entries (-1) add nothing.
+__global__ void k_seed_prev(BestEntry* __restrict__ best, const double* __restrict__ B,
+                            const double* __restrict__ cmp_old, const int64_t* __restrict__ idx_old,
+                            int l_old) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l_old; i += gridDim.x * blockDim.x) {
+    if ((B && B[i] == 0.0) || idx_old[i] < 0) continue;
+    const BestEntry prev{static_cast<unsigned long long>(__double_as_longlong(cmp_old[i])), idx_old[i]};
+    const BestEntry cur = best[i];
+    if (lex_less(prev.v, prev.idx, cur.v, cur.idx)) best[i] = prev;
   }
-}
-
-__global__ void k_unreverse(const BestEntry* __restrict__ in, BestEntry* __restrict__ out, int L) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
-    out[i] = in[L - 1 - i];
 }
 
 // EngineState tail cursors: for completed diagonal k = excl + r, the window pair (pos, pos + k)
@@ -804,7 +788,7 @@ struct mprof_ctx {
   std::vector<int4> tiles_h;  // (first diagonal, first row, row end, -)
   int4* tiles_d = nullptr;
   size_t tiles_cap = 0;
-  long long tiles_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  long long tiles_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
   long long R_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // rows-per-tile choice cache
   long long R_val = 0;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
@@ -820,6 +804,7 @@ struct mprof_ctx {
   mprof_progress_fn progress = nullptr;  // anytime observer (band granularity)
   void* progress_user = nullptr;
   int form = MPROF_FORM_AUTO;             // filter-form override (mprof_ctx_set_form)
+  long long plan_R = 0;                   // rows per tile of the last planned series
   unsigned long long probe_replays = 0;   // last form probe: replayed blocks / sample cells
   double probe_cells = 0.0;
 };
@@ -835,13 +820,11 @@ struct mprof_state {
   size_t cmp_bytes = 0;
   int64_t* idx = nullptr;    // neighbours [L]
   size_t idx_bytes = 0;
-  double* rev = nullptr;     // reversed series scratch
-  size_t rev_bytes = 0;
-  void* fwd = nullptr;       // BestEntry scratch [L]
-  size_t fwd_bytes = 0;
   double* P = nullptr;       // finalized distances scratch [L]
   size_t P_bytes = 0;
   uint64_t done = 0;         // completed diagonals, ascending from cfg.exclusion (build may cancel)
+  long long plan_R = 0;      // the profile's sweep plan: rows per tile and kernel forms
+  int plan_flags = 0;
 };
 
 namespace {
@@ -912,7 +895,7 @@ void trim_ctx(mprof_ctx* c) {
   c->ws = c->io = nullptr;
   c->tiles_d = nullptr;
   c->ws_bytes = c->io_bytes = c->tiles_cap = 0;
-  std::fill(c->tiles_key, c->tiles_key + 8, -1LL);
+  std::fill(c->tiles_key, c->tiles_key + 9, -1LL);
   c->stats_t = nullptr;
 }
 
@@ -980,32 +963,62 @@ int32_t ensure_znorm_stats(mprof_ctx* c, const double* d_t, uint64_t n, const mp
   return MPROF_OK;
 }
 
-// rows-per-tile choice: exact mode aligns runs to refresh_interval (bit-exact reseeding points,
-// diag_scan.hpp:97-104) or runs whole diagonals; the fast mode balances seeding cost (m/(2R) of
-// the cell work) against having enough tiles for every SM.
-// Rows of diagonal block kb that hold cells: [0, min(L - kb, row_hi)).
-// Rows per tile of a diagonal block w < K diagonals wide (a band's last block): a narrow tile is
+// Profile length rounded up to 1/8 of its octave: the per-series plan (choose_R, probe_form) is
+// taken on it, so it does not change when a series grows a little.
+long long quantize_len(long long L) {
+  if (L <= 64) return L;
+  const int e = 63 - __builtin_clzll((unsigned long long)L);
+  const long long q = 1LL << (e - 3);
+  return (L + q - 1) / q * q;
+}
+
+// ---- tile geometry -----------------------------------------------------------------------------
+// Diagonals are cut into GLOBAL blocks of kK: [g0 + q kK, g0 + (q + 1) kK) ∩ [g0, L), with g0 the
+// first tile diagonal of a full sweep (exclusion + 1 in the fast mode, whose first-diagonal
+// prepass evaluates diagonal `exclusion`; exclusion in the exact mode). A band or an anytime chunk
+// sweeps the part of each global block it holds, and every diagonal k is seeded at the rows of one
+// grid that depends on the series only (rows per tile R from choose_R, shortened only for the
+// final narrow global block), so the arithmetic of every cell -- and therefore the profile, ties
+// included -- does not depend on how the diagonals are split across GPUs or chunks
+// (the reference: bit-identical for any thread count, tests/test_aamp.cpp:262-274).
+struct Grid {
+  long long L, g0, row_hi;  // profile length, grid origin, rows swept ([0, row_hi))
+  bool exact;
+  int m, S;                 // window, rows per shared-memory stage of the sweep policy
+  long long block_lo(long long k) const { return g0 + (k - g0) / kK * kK; }
+  long long block_hi(long long k) const { return std::min(L, block_lo(k) + kK); }
+};
+
+// Rows per tile of a global block w < kK diagonals wide (the final one): a narrow tile is
 // latency-bound per row (a thin tile of R rows costs ~3/4 of a full one), so its rows shrink with
 // its width. Exact mode keeps R: runs are seeded at multiples of refresh_interval.
-// S = the sweep policy's rows per shared-memory stage (stage_rows_for).
 long long block_R(long long R, long long w, bool exact, int S) {
   if (exact || w >= kK) return R;
   return std::min(R, std::max<long long>(2 * S, (R * w / kK + S - 1) / S * S));
 }
 
-long long count_tiles(int L, int k_lo, int k_hi, int row_hi, long long R, int S, bool exact = false) {
-  long long t = 0;
-  for (long long kb = k_lo; kb < k_hi; kb += kK) {
-    const long long Rb = block_R(R, std::min<long long>(kK, k_hi - kb), exact, S);
-    t += (std::min<long long>(L - kb, row_hi) + Rb - 1) / Rb;
+// Calls f(kb, ke, Rb) for every tile column: the part [kb, ke) of a global block inside the band
+// [k_lo, k_hi), with the block's rows per tile.
+template <class F>
+void for_columns(const Grid& g, long long k_lo, long long k_hi, long long R, F&& f) {
+  for (long long kb = k_lo; kb < k_hi;) {
+    const long long ke = std::min(k_hi, g.block_hi(kb));
+    f(kb, ke, block_R(R, g.block_hi(kb) - g.block_lo(kb), g.exact, g.S));
+    kb = ke;
   }
+}
+
+long long count_tiles(const Grid& g, long long k_lo, long long k_hi, long long R) {
+  long long t = 0;
+  for_columns(g, k_lo, k_hi, R, [&](long long kb, long long, long long Rb) {
+    t += (std::min<long long>(g.L - kb, g.row_hi) + Rb - 1) / Rb;
+  });
   return t;
 }
 
-// Cells of tile (kb, ra) (diagonals [kb, min(kb + K, k_hi)), rows [ra, min(ra + R, row_hi)),
-// diagonal k ends at row L - k): sum over k of clamp(min(A, B - k), 0), A = rows cap, B = L - ra.
-double tile_cells(long long L, long long kb, long long k_hi, long long row_hi, long long ra, long long R) {
-  const long long k0 = kb, k1 = std::min<long long>(kb + kK, k_hi);
+// Cells of the tile (diagonals [k0, k1), rows [ra, min(ra + R, row_hi)); diagonal k ends at row
+// L - k): sum over k of clamp(min(A, B - k), 0), A = rows cap, B = L - ra.
+double tile_cells(long long L, long long k0, long long k1, long long row_hi, long long ra, long long R) {
   const long long A = std::min(R, row_hi - ra), B = L - ra;
   if (A <= 0 || k0 >= k1) return 0.0;
   const long long kf = std::clamp(B - A, k0, k1);  // k < kf: full A rows
@@ -1015,29 +1028,33 @@ double tile_cells(long long L, long long kb, long long k_hi, long long row_hi, l
   return full + tri;
 }
 
-// The tile table in launch order, with each tile's modelled cost (row-steps of a full-width
-// tile: cells / K, with a per-row latency floor of a quarter row-step for narrow tiles, plus the
-// FP64 seeds, m per diagonal ~ 1/3 row-step each in FP64-pipe terms, and pipeline fill), in
-// diagonal-block order; the first block's tiles come first (they may run on the near-diagonal
-// side stream, dispatch_sweep). Longest-first ordering of the partial tiles was measured: +1 %
-// on C4 AAMP, -11 % on C3 (MPROF_TILE_ORDER_LPT keeps it available for experiments).
-void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, int m, int S,
-               std::vector<int4>& tiles, std::vector<double>* costs) {
+// The tile table of band [k_lo, k_hi) in launch order, int4 {first diagonal, first row, row end,
+// diagonal end}, with each tile's modelled cost (row-steps of a full-width tile: cells / K, with a
+// per-row latency floor of a quarter row-step for narrow tiles, plus the FP64 seeds, m per
+// diagonal ~ 1/3 row-step each in FP64-pipe terms, and pipeline fill), in diagonal order; the
+// columns of the global block next to the exclusion zone come first (they may run on the
+// near-diagonal side stream, dispatch_sweep). Longest-first ordering of the partial tiles was
+// measured: +1 % on C4 AAMP, -11 % on C3 (MPROF_TILE_ORDER_LPT keeps it for experiments).
+// l_old > 0 (an EngineState extension from profile length l_old): only the tiles that hold a cell
+// (i, i + k) with i + k >= l_old, i.e. a new window (row end re, column end ke: re + ke - 2 >=
+// l_old); they are the fresh sweep's own tiles, so every cell keeps its fresh-sweep arithmetic.
+void tile_list(const Grid& g, long long k_lo, long long k_hi, long long R, std::vector<int4>& tiles,
+               std::vector<double>* costs, long long l_old = 0) {
   tiles.clear();
   std::vector<double> cost;
-  const double fixed = (double)m / 3.0 + 2.0 * S;
+  const double fixed = (double)g.m / 3.0 + 2.0 * g.S;
   size_t first_block = 0;
-  for (long long kb = k_lo; kb < k_hi; kb += kK) {
-    const long long w = std::min<long long>(kK, k_hi - kb);
-    const long long rend = std::min<long long>(L - kb, row_hi);
-    const long long Rb = block_R(R, w, exact, S);
+  for_columns(g, k_lo, k_hi, R, [&](long long kb, long long ke, long long Rb) {
+    const long long rend = std::min<long long>(g.L - kb, g.row_hi);
     for (long long ra = 0; ra < rend; ra += Rb) {
-      tiles.push_back(make_int4((int)kb, (int)ra, (int)std::min(ra + Rb, rend), 0));
-      const double cells = tile_cells(L, kb, k_hi, row_hi, ra, Rb);
-      cost.push_back(std::max(cells / kK, cells / w * 0.25) + fixed);
+      const long long re = std::min(ra + Rb, rend);
+      if (l_old > 0 && re + ke - 2 < l_old) continue;
+      tiles.push_back(make_int4((int)kb, (int)ra, (int)re, (int)ke));
+      const double cells = tile_cells(g.L, kb, ke, g.row_hi, ra, Rb);
+      cost.push_back(std::max(cells / kK, cells / (double)(ke - kb) * 0.25) + fixed);
     }
     if (kb == k_lo) first_block = tiles.size();
-  }
+  });
   if (knobs().tile_order_lpt) {  // experiments: decreasing cost after the first block
     std::vector<size_t> ord(tiles.size());
     for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
@@ -1055,14 +1072,12 @@ void tile_list(int L, int k_lo, int k_hi, int row_hi, long long R, bool exact, i
   if (costs) costs->swap(cost);
 }
 
-// Makespan (in row-steps of a full-width tile) of the tile list in launch order on `slots`
-// resident CTAs: the block scheduler hands the next tile to the first free slot (list
-// scheduling).
-double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int slots, int m,
-                         int S) {
+// Makespan (in row-steps of a full-width tile) of the band's tile list in launch order on `slots`
+// resident CTAs: the block scheduler hands the next tile to the first free slot (list scheduling).
+double schedule_makespan(const Grid& g, long long k_lo, long long k_hi, long long R, int slots) {
   std::vector<int4> tiles;
   std::vector<double> cost;
-  tile_list(L, k_lo, k_hi, row_hi, R, false, m, S, tiles, &cost);
+  tile_list(g, k_lo, k_hi, R, tiles, &cost);
   std::vector<double> heap(slots, 0.0);  // min-heap of slot free times
   auto cmp = std::greater<double>();
   double makespan = 0.0;
@@ -1075,52 +1090,77 @@ double schedule_makespan(int L, int k_lo, int k_hi, int row_hi, long long R, int
   return makespan;
 }
 
-// Rows per tile. Longest runs amortise the seeds best (R_max = 32 m rows), but a grid of a few
-// waves loses up to a whole wave to its tail: the candidates R_max / j (stage multiples) are
-// scheduled on the sweep kernel's real residency (slots = occupancy x SMs) and the shortest
-// makespan wins (ties -> longer tiles). Grids of >= 16 waves keep R_max (tail < ~3 %). The
-// choice is cached per context and shape (the simulation costs up to a few ms of host time).
-long long choose_R(const mprof_config* cfg, int L, int k_lo, int k_hi, int row_hi, int slots,
-                   int S) {
+// Rows per tile of a series (one value for every band, chunk and GPU count: see Grid). Exact mode
+// aligns runs to refresh_interval (the reference's refresh points, diag_scan.hpp:97-104) or runs
+// whole diagonals. Fast mode: the longest runs amortise the seeds best (R_max = 32 m rows, seeds
+// <= ~1.6 % of the FP64 work), but a grid of a few waves loses up to a whole wave to its tail.
+// Grids that still hold >= 16 waves of resident CTAs when split into kPlanBands equal-area bands
+// keep R_max; otherwise the candidates R_max / j (stage multiples) are list-scheduled on the
+// kernel's real residency (slots = occupancy x SMs) both for the whole sweep on one GPU (M1) and
+// for the slowest of kPlanBands bands (M8), and the candidate with the smallest M8 among those
+// within 1 % of the best M1 wins (ties -> longer tiles). The model runs on the profile length
+// rounded up to 1/8 of its octave, so a series that grows a little (an EngineState extension)
+// keeps its R and is extended incrementally. Cached per context and shape.
+constexpr int kPlanBands = 8;
+long long choose_R(const mprof_config* cfg, const Grid& gx, int slots) {
+  Grid g = gx;
+  if (!cfg->exact && g.row_hi == g.L) g.L = g.row_hi = quantize_len(g.L);
   if (cfg->exact) {
     if (cfg->refresh_interval > 0) return (long long)cfg->refresh_interval;
-    return L;  // the whole diagonal is one run, like the reference's refresh = 0
+    return g.L;  // the whole diagonal is one run, like the reference's refresh = 0
   }
+  const int S = g.S;
   long long Rmax = std::max<long long>(32LL * (long long)cfg->m, 8LL * S);
   Rmax = (Rmax + S - 1) / S * S;
   if (cfg->refresh_interval > 0) Rmax = std::min<long long>(Rmax, (long long)cfg->refresh_interval);
-  long long R = Rmax;
   if (knobs().rows_per_tile) return knobs().rows_per_tile;  // experiments
-  if (Rmax > 2 * S && count_tiles(L, k_lo, k_hi, row_hi, Rmax, S) < 16LL * slots) {
-    double best = schedule_makespan(L, k_lo, k_hi, row_hi, Rmax, slots, (int)cfg->m, S);
-    long long prev = Rmax;
-    for (int j = 2; j <= 32; ++j) {
-      const long long Rj = std::max<long long>(2 * S, (Rmax / j + S - 1) / S * S);
-      if (Rj >= prev) continue;
-      prev = Rj;
-      if (count_tiles(L, k_lo, k_hi, row_hi, Rj, S) > 32LL * slots) break;
-      const double ms = schedule_makespan(L, k_lo, k_hi, row_hi, Rj, slots, (int)cfg->m, S);
-      if (knobs().tile_debug)
-        fprintf(stderr, "[mprof tiles] slots %d R %lld tiles %lld makespan %.0f (R_max %.0f)\n", slots,
-                Rj, count_tiles(L, k_lo, k_hi, row_hi, Rj, S), ms, best);
-      if (ms < best * (1.0 - 1e-3)) {
-        best = ms;
-        R = Rj;
-      }
-      if (Rj == 2 * S) break;
+  const long long k_lo = g.g0, k_hi = g.L;
+  if (k_lo >= k_hi || Rmax <= 2 * S ||
+      count_tiles(g, k_lo, k_hi, Rmax) >= 16LL * kPlanBands * slots)
+    return Rmax;
+  std::vector<uint64_t> cuts(kPlanBands + 1);
+  const uint64_t n = (uint64_t)(g.L + g.m - 1);
+  if (mprof_band_cuts(n, (uint64_t)g.m, (uint64_t)cfg->exclusion, kPlanBands, cuts.data()) != MPROF_OK)
+    return Rmax;
+  struct Cand { long long R; double m1, m8; };
+  std::vector<Cand> cand;
+  long long prev = 0;
+  for (int j = 1; j <= 32; ++j) {
+    const long long Rj = j == 1 ? Rmax : std::max<long long>(2 * S, (Rmax / j + S - 1) / S * S);
+    if (prev && Rj >= prev) continue;
+    prev = Rj;
+    if (j > 1 && count_tiles(g, k_lo, k_hi, Rj) > 32LL * kPlanBands * slots) break;
+    Cand c{Rj, schedule_makespan(g, k_lo, k_hi, Rj, slots), 0.0};
+    for (int b = 0; b < kPlanBands; ++b) {
+      const long long a = std::max<long long>((long long)cuts[b], k_lo), z = (long long)cuts[b + 1];
+      if (a < z) c.m8 = std::max(c.m8, schedule_makespan(g, a, z, Rj, slots));
     }
+    if (knobs().tile_debug)
+      fprintf(stderr, "[mprof tiles] slots %d R %lld tiles %lld M1 %.0f M8 %.0f\n", slots, Rj,
+              count_tiles(g, k_lo, k_hi, Rj), c.m1, c.m8);
+    cand.push_back(c);
+    if (Rj == 2 * S) break;
   }
+  double best_m1 = cand[0].m1;
+  for (const Cand& c : cand) best_m1 = std::min(best_m1, c.m1);
+  long long R = Rmax;
+  double best_m8 = INFINITY;
+  for (const Cand& c : cand)  // descending R: a later candidate must be strictly better
+    if (c.m1 <= best_m1 * 1.01 && c.m8 < best_m8 * (1.0 - 1e-3)) {
+      best_m8 = c.m8;
+      R = c.R;
+    }
   return R;
 }
 
-int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long long R, bool exact,
-                    int m, int S, long long* ntiles) {
-  const long long key[8] = {L, k_lo, k_hi, R, exact ? -kK : kK, row_hi, m, S};
-  if (std::equal(key, key + 8, c->tiles_key)) {
+int32_t build_tiles(mprof_ctx* c, const Grid& g, long long k_lo, long long k_hi, long long R,
+                    long long l_old, long long* ntiles) {
+  const long long key[9] = {g.L, k_lo, k_hi, R, g.exact ? -g.g0 : g.g0, g.row_hi, g.m, g.S, l_old};
+  if (std::equal(key, key + 9, c->tiles_key)) {
     *ntiles = (long long)c->tiles_h.size();
     return MPROF_OK;
   }
-  tile_list(L, k_lo, k_hi, row_hi, R, exact, m, S, c->tiles_h, nullptr);
+  tile_list(g, k_lo, k_hi, R, c->tiles_h, nullptr, l_old);
   const size_t need = c->tiles_h.size() * sizeof(int4);
   void* p = c->tiles_d;
   int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
@@ -1128,7 +1168,7 @@ int32_t build_tiles(mprof_ctx* c, int L, int k_lo, int k_hi, int row_hi, long lo
   if (st != MPROF_OK) return st;
   CK(cudaMemcpyAsync(c->tiles_d, c->tiles_h.data(), need, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // tiles_h may be rebuilt by the next call
-  std::copy(key, key + 8, c->tiles_key);
+  std::copy(key, key + 9, c->tiles_key);
   *ntiles = (long long)c->tiles_h.size();
   return MPROF_OK;
 }
@@ -1202,7 +1242,11 @@ int32_t with_policy(const mprof_ctx* c, const mprof_config* cfg, F&& f) {
   if (p == 1.0) return ex ? f.template operator()<Pnorm<1, true>>() : f.template operator()<Pnorm<1, false>>();
   if (p == 3.0) return ex ? f.template operator()<Pnorm<3, true>>() : f.template operator()<Pnorm<3, false>>();
   if (p == 4.0) return ex ? f.template operator()<Pnorm<4, true>>() : f.template operator()<Pnorm<4, false>>();
-  return ex ? f.template operator()<Pnorm<0, true>>() : f.template operator()<Pnorm<0, false>>();
+  if (ex) return f.template operator()<Pnorm<0, true>>();
+  if (p == 1.5) return f.template operator()<Pnorm<-3, false>>();
+  if (p == 2.5) return f.template operator()<Pnorm<-5, false>>();
+  if (p == 3.5) return f.template operator()<Pnorm<-7, false>>();
+  return f.template operator()<Pnorm<0, false>>();
 }
 
 // Side stream + fork/join events (created on first use).
@@ -1227,20 +1271,24 @@ int32_t ensure_side(mprof_ctx* c) {
 // band's diagonal blocks and rows are swept with the covariance kernel (after the first-diagonal
 // pass, so the thresholds are the real ones) with a replay counter. The probe cells are genuine
 // cells of the band (offers are exact minima, so sweeping them again later changes nothing).
+// The sample's geometry is taken on the quantized profile length (quantize_len), so a series that
+// grows a little (an EngineState extension) samples the same tiles and keeps its decision.
 int32_t probe_form(mprof_ctx* c, bool zn, const SweepParams& prm, int kb_lo, uint32_t* launches) {
   const int L = prm.L, k_hi = prm.k_hi, row_hi = prm.row_hi;
-  const long long nblk = (k_hi - kb_lo + kK - 1) / kK;
+  const long long Lq = quantize_len(L);
+  const long long nblk = (Lq - kb_lo + kK - 1) / kK;
   if (nblk <= 0) return MPROF_OK;
   std::vector<int4> pt;
   double cells = 0.0;
   for (int q = 0; q < kProbeTiles; ++q) {
     const long long kb = kb_lo + kK * ((long long)q * nblk / kProbeTiles);
     const long long rend = std::min<long long>(L - kb, row_hi);
-    if (rend <= 0) continue;
-    const long long span = std::max<long long>(1, rend - kProbeRows);
+    if (kb >= k_hi || rend <= 0) continue;
+    const long long span = std::max<long long>(1, Lq - kb - kProbeRows);
     const long long ra = (long long)(((unsigned long long)q * 2654435761ull) % (unsigned long long)span);
+    if (ra >= rend) continue;
     const long long re = std::min<long long>(ra + kProbeRows, rend);
-    pt.push_back(make_int4((int)kb, (int)ra, (int)re, 0));
+    pt.push_back(make_int4((int)kb, (int)ra, (int)re, (int)std::min<long long>(kb + kK, k_hi)));
     cells += (double)(re - ra) * (double)std::min<long long>(kK, k_hi - kb);
   }
   if (pt.empty() || cells <= 0.0) return MPROF_OK;
@@ -1440,29 +1488,14 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
 }
 
 // (2) the tiles of diagonals [k_lo, k_hi) x rows [0, row_hi) into w.best (initialised by the
-// caller); rl > 0: reflected sweep (indices stored as rl - 1 - idx)
+// caller)
 struct SweepOut {
   float ms = 0.f;
   long long ntiles = 0, R = 0;
 };
 
-// first_diag: seed the filter thresholds with diagonal `exclusion` (evaluated directly). Those are
-// genuine cells even when the band starts further out, so band profiles still merge exactly, and
-// every band starts from near-final thresholds (random walks: ~all nearest neighbours at k = 1).
-int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
-                    const Workspace& w, int k_lo, int k_hi, int row_hi, int rl, bool first_diag,
-                    uint32_t* launches, SweepOut* out) {
-  const int m = (int)cfg->m;
-  const int L = n - m + 1;
-  if (k_lo >= k_hi || row_hi <= 0) return MPROF_OK;
-  first_diag = first_diag && !cfg->exact;
-  // Diagonal `exclusion` is evaluated directly by the prepass; sweeping it again in the tiles
-  // would re-offer values equal to the thresholds they set (every block of those lanes replays
-  // and pays L2 round trips: the first diagonal block becomes the critical path of a band).
-  const int k_tile = (first_diag && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
-  c->wide = c->form == MPROF_FORM_WIDE;  // else set by the form probe below
-  c->probe_replays = 0;
-  c->probe_cells = 0.0;
+SweepParams make_params(const mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
+                        const Workspace& w, int k_hi, int row_hi) {
   SweepParams prm;
   prm.t = d_t;
   prm.A = w.A;
@@ -1476,68 +1509,123 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   prm.best = w.best;
   prm.tiles = nullptr;
   prm.n = n;
-  prm.m = m;
-  prm.L = L;
+  prm.m = (int)cfg->m;
+  prm.L = n - (int)cfg->m + 1;
   prm.k_hi = k_hi;
   prm.R = 0;
   prm.row_hi = row_hi;
-  prm.rl = rl;
   prm.p = cfg->p;
   prm.stats = nullptr;
   prm.scratch = w.cv;
-  // Confirm an automatically chosen covariance-only form (AAMP or z-norm) on the series itself (full sweeps of
-  // large bands): the first-diagonal thresholds, then the probe, then the tiling for the kernel
-  // that will run.
+  return prm;
+}
+
+Grid grid_of(const mprof_ctx* c, const mprof_config* cfg, int L, int row_hi) {
+  return Grid{L, (long long)cfg->exclusion + (cfg->exact ? 0 : 1), row_hi, cfg->exact != 0,
+              (int)cfg->m, stage_rows_for(c, cfg)};
+}
+
+// Per-series decisions, taken once before any band / chunk is swept so that they are the same
+// for every band of a multi-GPU run and every chunk of an anytime run:
+//  * the filter form: an automatically chosen covariance-only form (AAMP or z-norm) is confirmed
+//    on the series itself when the WHOLE sweep has >= kProbeMinCells cells: the first-diagonal
+//    thresholds, then the probe over the whole diagonal range (probe_form);
+//  * the rows per tile (choose_R on the whole range).
+struct SeriesPlan {
+  long long R = 0;
+  bool first_diag_done = false;  // the prepass of diagonal `exclusion` already ran
+};
+
+int32_t plan_series(mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
+                    const Workspace& w, int row_hi, uint32_t* launches, SeriesPlan* out) {
+  const int L = n - (int)cfg->m + 1;
+  c->wide = c->form == MPROF_FORM_WIDE;  // else set by the form probe below
+  c->probe_replays = 0;
+  c->probe_cells = 0.0;
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
   const bool auto_cov = c->form == MPROF_FORM_AUTO &&
                         (zn ? (!c->zn_colscale && knobs().zn_filter == 0)
                             : (c->aamp_cov && knobs().aamp_cov == -1));
-  if (auto_cov && !cfg->exact && cfg->precision == MPROF_FP64 && rl == 0 && row_hi == L &&
-      k_hi - k_tile > 2 * kK &&
-      (double)mprof_band_cells((uint64_t)n, (uint64_t)m, (uint64_t)k_tile, (uint64_t)k_hi) >= kProbeMinCells) {
-    if (first_diag) {
-      int32_t st = with_policy(c, cfg, [&]<class P>() {
-        return launch_first_diag<P>(c, prm, (int)cfg->exclusion, launches);
-      });
-      if (st != MPROF_OK) return st;
-      first_diag = false;
-    }
-    int32_t st = probe_form(c, zn, prm, k_tile + kK, launches);
+  const long long g0 = (long long)cfg->exclusion + 1;
+  const bool big = row_hi == L && L - g0 > 2 * kK &&
+                   (double)mprof_band_cells((uint64_t)n, cfg->m, (uint64_t)g0, (uint64_t)L) >= kProbeMinCells;
+  if (auto_cov && !cfg->exact && cfg->precision == MPROF_FP64 && !big) {
+    // Below the probe size the covariance-only forms are not used: their block bound's slack is
+    // unconfirmed and small sweeps measured slower with them (random walk n = 2^16, m = 256:
+    // EuclidCov 1.76 ms vs (delta, sigma) 0.76 ms; Znorm<0> 0.33 vs Znorm<1> 0.12 ms at n = 2^14).
+    if (zn) c->zn_colscale = true;
+    else c->aamp_cov = false;
+  }
+  if (auto_cov && !cfg->exact && cfg->precision == MPROF_FP64 && big) {
+    const SweepParams prm = make_params(c, d_t, n, cfg, w, L, L);
+    int32_t st = with_policy(c, cfg, [&]<class P>() {
+      return launch_first_diag<P>(c, prm, (int)cfg->exclusion, launches);
+    });
     if (st != MPROF_OK) return st;
-    if (!zn && !c->aamp_cov) prm.mu = w.mu;
+    out->first_diag_done = true;
+    st = probe_form(c, zn, prm, (int)(g0 + kK), launches);
+    if (st != MPROF_OK) return st;
   }
-  const int S = stage_rows_for(c, cfg);
-  {
-    long long pbits;
-    std::memcpy(&pbits, &cfg->p, sizeof pbits);
-    const long long key[9] = {L, k_tile, k_hi, row_hi, (long long)cfg->m, cfg->exact,
-                              (long long)cfg->refresh_interval,
-                              ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) | (c->aamp_cov ? 2 : 0) | (c->wide ? 4 : 0),
-                              pbits};
-    if (std::equal(key, key + 9, c->R_key)) {
-      out->R = c->R_val;
-    } else {
-      out->R = choose_R(cfg, L, k_tile, k_hi, row_hi, c->num_sms * sweep_blocks_per_sm(c, cfg), S);
-      if (!knobs().rows_per_tile) {
-        std::copy(key, key + 9, c->R_key);
-        c->R_val = out->R;
-      }
+  const Grid g = grid_of(c, cfg, L, row_hi);
+  long long pbits;
+  std::memcpy(&pbits, &cfg->p, sizeof pbits);
+  const int slots = c->num_sms * sweep_blocks_per_sm(c, cfg);
+  const long long key[9] = {L, g.g0, row_hi, (long long)cfg->m, cfg->exact,
+                            (long long)cfg->refresh_interval,
+                            ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) |
+                                (c->aamp_cov ? 2 : 0) | (c->wide ? 4 : 0),
+                            pbits, slots};
+  if (std::equal(key, key + 9, c->R_key)) {
+    out->R = c->R_val;
+  } else {
+    out->R = choose_R(cfg, g, slots);
+    if (!knobs().rows_per_tile) {
+      std::copy(key, key + 9, c->R_key);
+      c->R_val = out->R;
     }
   }
-  int32_t st = build_tiles(c, L, k_tile, k_hi, row_hi, out->R, cfg->exact != 0, m, S, &out->ntiles);
+  c->plan_R = out->R;
+  return MPROF_OK;
+}
+
+// The per-series decisions that fix every cell's arithmetic: rows per tile and kernel forms.
+int plan_flags(const mprof_ctx* c) {
+  return (c->aamp_cov ? 1 : 0) | (c->zn_colscale ? 2 : 0) | (c->wide ? 4 : 0);
+}
+
+// The tiles of diagonals [k_lo, k_hi) x rows [0, row_hi) into w.best (initialised by the caller),
+// R rows per tile (plan_series).
+// first_diag: seed the filter thresholds with diagonal `exclusion` (evaluated directly) first.
+// Those are genuine cells even when the band starts further out, so band profiles still merge
+// exactly, and every band starts from near-final thresholds (random walks: ~all nearest
+// neighbours at k = 1). In the fast mode diagonal `exclusion` belongs to that prepass, never to
+// the tiles (tile grid origin exclusion + 1): sweeping it again would re-offer values equal to
+// the thresholds it set (every block of those lanes replays and pays L2 round trips).
+int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
+                    const Workspace& w, int k_lo, int k_hi, int row_hi, bool first_diag,
+                    long long R, long long l_old, uint32_t* launches, SweepOut* out) {
+  const int L = n - (int)cfg->m + 1;
+  if (k_lo >= k_hi || row_hi <= 0) return MPROF_OK;
+  first_diag = first_diag && !cfg->exact;
+  const int k_tile = (!cfg->exact && k_lo == (int)cfg->exclusion) ? k_lo + 1 : k_lo;
+  SweepParams prm = make_params(c, d_t, n, cfg, w, k_hi, row_hi);
+  const Grid g = grid_of(c, cfg, L, row_hi);
+  out->R = R;
+  int32_t st = build_tiles(c, g, k_tile, k_hi, R, l_old, &out->ntiles);
   if (st != MPROF_OK) return st;
   prm.tiles = c->tiles_d;
-  prm.R = (int)std::min<long long>(out->R, INT_MAX);
+  prm.R = (int)std::min<long long>(R, INT_MAX);
   const bool want_stats = knobs().stats;
   if (want_stats) {
     CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
   }
+  // the global block next to the exclusion zone runs the side kernel (dispatch_sweep)
   long long n_near = 0;
   const bool cov_main = (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale) ||
                         (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov);
-  if (cov_main && !cfg->exact && k_tile <= (int)cfg->exclusion + 1 && !knobs().zn_no_near)
-    n_near = count_tiles(L, k_tile, std::min(k_tile + kK, k_hi), row_hi, out->R, S);  // first block
+  if (cov_main && !cfg->exact && !knobs().zn_no_near)  // the list is in ascending diagonal order
+    while (n_near < out->ntiles && c->tiles_h[n_near].x < g.g0 + kK) ++n_near;
   st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
                       &out->ms);
   if (st != MPROF_OK) return st;
@@ -1547,7 +1635,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     CK(cudaStreamSynchronize(c->stream));
     cudaFreeAsync(prm.stats, c->stream);
     fprintf(stderr, "[mprof stats] family %d L %d tiles %lld R %lld: replays %llu offers %llu\n",
-            cfg->family, L, out->ntiles, out->R, h[0], h[1]);
+            cfg->family, L, out->ntiles, R, h[0], h[1]);
   }
   return MPROF_OK;
 }
@@ -1624,8 +1712,12 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
   ++launches;
   SweepOut so;
   long long k_done = k_hi;
+  SeriesPlan plan;
+  st = plan_series(c, d_t, n, cfg, w, L, &launches, &plan);
+  if (st != MPROF_OK) return st;
   if (!c->progress || k_lo >= k_hi) {
-    st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, 0, true, &launches, &so);
+    st = sweep_tiles(c, d_t, n, cfg, w, (int)k_lo, (int)k_hi, L, !plan.first_diag_done, plan.R, 0,
+                     &launches, &so);
     if (st != MPROF_OK) return st;
   } else {
     // Anytime mode (scan_diagonals' observer, /root/reference/proj/src/detail/diag_scan.hpp:
@@ -1637,7 +1729,8 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
     for (long long a = k_lo; a < k_hi; a += chunk) {
       const long long b = std::min(k_hi, a + chunk);
       SweepOut part;
-      st = sweep_tiles(c, d_t, n, cfg, w, (int)a, (int)b, L, 0, a == k_lo, &launches, &part);
+      st = sweep_tiles(c, d_t, n, cfg, w, (int)a, (int)b, L, a == k_lo && !plan.first_diag_done,
+                       plan.R, 0, &launches, &part);
       if (st != MPROF_OK) return st;
       so.ms += part.ms;
       so.ntiles += part.ntiles;
@@ -2230,6 +2323,8 @@ int32_t mprof_state_build(mprof_ctx* in, const double* t, uint64_t n, const mpro
   c->progress_user = nullptr;
   if (st != MPROF_OK) { mprof_state_destroy(S); return st; }
   S->done = (info ? info : &local)->diagonals;
+  S->plan_R = c->plan_R;
+  S->plan_flags = plan_flags(c);
   trim_ctx(c);
   *out = S;
   return MPROF_OK;
@@ -2272,49 +2367,59 @@ int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count
     S->t_bytes = cap;
   }
   CK(cudaMemcpyAsync(S->t + n_old, samples, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  st = ensure(reinterpret_cast<void**>(&S->rev), &S->rev_bytes, n_new * sizeof(double));
-  if (st == MPROF_OK) st = ensure(&S->fwd, &S->fwd_bytes, (size_t)L_new * sizeof(BestEntry));
-  if (st != MPROF_OK) return st;
+  // The extended series is planned exactly as a fresh build would plan it (operands, form probe,
+  // rows per tile). When that plan equals the one the stored profile was swept with, every old
+  // cell already has its fresh-sweep value: the old entries seed the profile and only the fresh
+  // sweep's tiles that hold a new window's cells run (tile_list, l_old), so the result is
+  // bit-identical to a fresh profile of the extended series (extend_profile's contract,
+  // /root/reference/proj/include/mprof/engine_state.hpp:47-52). Otherwise the whole extended
+  // series is swept.
   uint32_t launches = 0;
-  k_reverse<<<grid_for((long long)n_new), 256, 0, c->stream>>>(S->t, S->rev, (int)n_new);
-  ++launches;
-  // sweep the new cells: rows [0, dL) of every diagonal of the reversed series
   Workspace w;
   st = carve(c, L_new, &w);
   if (st != MPROF_OK) return st;
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
-  st = prepare_operands(c, S->rev, (int)n_new, cfg, w, &launches);
+  st = prepare_operands(c, S->t, (int)n_new, cfg, w, &launches);
   if (st != MPROF_OK) return st;
-  k_init_from_prev<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, S->cmp, S->idx,
-                                                            L_old, L_new);
+  k_init_best<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, L_new);
   ++launches;
+  SeriesPlan plan;
+  st = plan_series(c, S->t, (int)n_new, cfg, w, L_new, &launches, &plan);
+  if (st != MPROF_OK) return st;
+  const bool incremental = plan.R == S->plan_R && plan_flags(c) == S->plan_flags;
+  if (incremental) {
+    k_seed_prev<<<grid_for(L_old), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, S->cmp, S->idx, L_old);
+    ++launches;
+  }
   SweepOut so;
   const int k_lo = (int)cfg->exclusion;
-  st = sweep_tiles(c, S->rev, (int)n_new, cfg, w, k_lo, L_new, dL, L_new, true, &launches, &so);
+  st = sweep_tiles(c, S->t, (int)n_new, cfg, w, k_lo, L_new, L_new, !plan.first_diag_done, plan.R,
+                   incremental ? L_old : 0, &launches, &so);
   if (st != MPROF_OK) return st;
-  BestEntry* fwd = static_cast<BestEntry*>(S->fwd);
-  k_unreverse<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, fwd, L_new);
-  ++launches;
   if (zn) {
-    st = ensure_znorm_stats(c, S->t, n_new, cfg, w);  // forward statistics (stats key differs)
+    st = flat_fix(c, w.B, L_new, k_lo, L_new, w, w.best, &launches);
     if (st != MPROF_OK) return st;
-    st = flat_fix(c, w.B, L_new, k_lo, L_new, w, fwd, &launches);
-    if (st != MPROF_OK) return st;
-    ++launches;
   }
   st = ensure(reinterpret_cast<void**>(&S->cmp), &S->cmp_bytes, (size_t)L_new * sizeof(double));
   if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&S->idx), &S->idx_bytes, (size_t)L_new * sizeof(int64_t));
   if (st != MPROF_OK) return st;
-  k_split<<<grid_for(L_new), 256, 0, c->stream>>>(fwd, S->cmp, S->idx, L_new);
+  k_split<<<grid_for(L_new), 256, 0, c->stream>>>(w.best, S->cmp, S->idx, L_new);
   ++launches;
   CK(cudaGetLastError());
   S->n = n_new;
   S->done = state_total(S);
-  trim_ctx(c);
-  // cells swept: diagonals k in [excl, L_new) contribute min(dL, L_new - k)
+  S->plan_R = plan.R;
+  S->plan_flags = plan_flags(c);
+  // cells swept: the tiles' cells (incremental) or the whole extended series
   uint64_t cells = 0;
-  for (long long k = k_lo; k < L_new; ++k) cells += (uint64_t)std::min<long long>(dL, L_new - k);
+  if (incremental) {
+    for (const int4& tl : c->tiles_h)
+      cells += (uint64_t)tile_cells(L_new, tl.x, tl.w, L_new, tl.y, tl.z - tl.y);
+  } else {
+    cells = mprof_band_cells(n_new, cfg->m, cfg->exclusion, (uint64_t)L_new);
+  }
   fill_info(c, cfg, cells, L_new - k_lo, so, launches, info);
+  trim_ctx(c);
   return MPROF_OK;
 }
 
@@ -2329,6 +2434,8 @@ int32_t mprof_state_clone(const mprof_state* S, mprof_state** out) {
   R->cfg = S->cfg;
   R->n = S->n;
   R->done = S->done;
+  R->plan_R = S->plan_R;
+  R->plan_flags = S->plan_flags;
   const uint64_t L = S->n - S->cfg.m + 1;
   int32_t st = ensure(reinterpret_cast<void**>(&R->t), &R->t_bytes, S->n * sizeof(double));
   if (st == MPROF_OK) st = ensure(reinterpret_cast<void**>(&R->cmp), &R->cmp_bytes, L * sizeof(double));
@@ -2379,8 +2486,6 @@ void mprof_state_destroy(mprof_state* S) {
   cudaFree(S->t);
   cudaFree(S->cmp);
   cudaFree(S->idx);
-  cudaFree(S->rev);
-  cudaFree(S->fwd);
   cudaFree(S->P);
   mprof_ctx_destroy(S->ctx);
   delete S;

@@ -31,6 +31,12 @@
 
 namespace mpg {
 
+// Rows of a replayed block unrolled per iteration (replay_block; 1 = rolled, D = fully unrolled).
+#ifndef MPROF_REPLAY_UNROLL
+#define MPROF_REPLAY_UNROLL 1
+#endif
+constexpr int kReplayUnroll = MPROF_REPLAY_UNROLL;
+
 // ---------------------------------------------------------------------------------------------
 // Global profile entry: comparison-space value bits (non-negative double or +inf) and index.
 struct __align__(16) BestEntry {
@@ -48,11 +54,13 @@ __device__ __forceinline__ bool lex_less(unsigned long long v, long long i, unsi
 
 // Exact lexicographic min-update of best[pos] with (v, idx); returns the resulting value bits.
 // MinBuffer::update (/root/reference/proj/src/detail/diag_scan.hpp:37-43) as a lock-free
-// 128-bit CAS loop. The initial 16-byte read is not guaranteed single-copy atomic: a torn read
-// that makes the entry look smaller than it is (e.g. the new value with the old, smaller index)
-// would drop a valid offer. So a "no improvement" verdict is only returned after an atomic
-// snapshot (a CAS that writes back what it compares with) confirmed the entry it was based on;
-// an improving offer is decided by its own CAS.
+// 128-bit CAS loop. The initial 16-byte read is not guaranteed single-copy atomic as a whole
+// (each aligned 8-byte word is): it may pair a value with the index of an older or newer entry.
+// Entries only decrease, so a read value word above v, or below it, decides the offer on its own
+// (below: no improvement; above: the CAS decides); only an exact value tie depends on the index,
+// and a torn read there (the new value with the old, smaller index) could drop a valid offer, so
+// a tie verdict of "no improvement" is confirmed by an atomic snapshot (a CAS that writes back
+// what it compares with).
 __device__ __forceinline__ unsigned long long offer(BestEntry* best, long long pos,
                                                     unsigned long long v, long long idx) {
   const longlong2 raw = __ldcg(reinterpret_cast<const longlong2*>(best + pos));
@@ -64,7 +72,7 @@ __device__ __forceinline__ unsigned long long offer(BestEntry* best, long long p
       if (old.v == cur.v && old.idx == cur.idx) return v;
       cur = old;
     } else {
-      if (atomic_read) return cur.v;
+      if (atomic_read || cur.v != v) return cur.v;
       const BestEntry snap = atomicCAS(best + pos, cur, cur);
       if (snap.v == cur.v && snap.idx == cur.idx) return cur.v;
       cur = snap;
@@ -165,11 +173,34 @@ __device__ __forceinline__ double abs_pow_exact(double x, double p) {
   if constexpr (PK == 1) return a;
   else if constexpr (PK == 3) return __dmul_rn(__dmul_rn(a, a), a);
   else if constexpr (PK == 4) return __dmul_rn(__dmul_rn(a, a), __dmul_rn(a, a));
-  else return pow(a, p);
+  else return pow(a, p);  // generic and half-integer p: std::pow, as the reference
 }
 
-// p-norm AAMP: accumulator sum |t_i - t_j|^p. PK = 1, 3, 4 integer fast paths; 0 = generic pow.
-// Reference: incremental_pnorm_step (aamp.hpp:45-49), direct_pnorm_acc (diag_scan.hpp:66-71).
+// a^p (a >= 0) in the fast mode. PK = 1, 3, 4: exact products; PK = -k: the half-integer
+// p = k / 2 (k odd) as a^((k-1)/2) sqrt(a) (sqrt is correctly rounded: ~10 FP64-pipe
+// instructions instead of pow's ~100); PK = 0, any other p: exp2(p log2 a), relative error
+// ~ |p log2 a| 1e-16 against pow's ~1e-16 (the profile's tolerance is 1e-9).
+template <int PK>
+__device__ __forceinline__ double pow_fast(double a, double p) {
+  if constexpr (PK == 1) return a;
+  else if constexpr (PK == 3) return a * a * a;
+  else if constexpr (PK == 4) { const double a2 = a * a; return a2 * a2; }
+  else if constexpr (PK < 0) {
+    constexpr int h = (-PK - 1) / 2;  // integer part of p
+    const double r = sqrt(a);
+    if constexpr (h == 0) return r;
+    else if constexpr (h == 1) return a * r;
+    else if constexpr (h == 2) return (a * a) * r;
+    else return (a * a) * (a * r);
+  } else {
+    return a == 0.0 ? 0.0 : exp2(p * log2(a));
+  }
+}
+
+// p-norm AAMP: accumulator sum |t_i - t_j|^p. PK = 1, 3, 4 integer fast paths, PK = -3, -5, -7 the
+// half-integers p = 1.5, 2.5, 3.5 (fast mode; the exact mode evaluates them with pow like the
+// reference), 0 = generic p. Reference: incremental_pnorm_step (aamp.hpp:45-49), direct_pnorm_acc
+// (diag_scan.hpp:66-71).
 template <int PK, bool EXACT>
 struct Pnorm : KeyF64 {
   using Base = Pnorm;
@@ -199,7 +230,7 @@ struct Pnorm : KeyF64 {
         const double o2 = out * out, i2 = in * in;
         return fma(i2, i2, fma(-o2, o2, acc));
       } else {
-        return (acc - pow(fabs(out), p)) + pow(fabs(in), p);
+        return (acc - pow_fast<PK>(fabs(out), p)) + pow_fast<PK>(fabs(in), p);
       }
     }
   }
@@ -212,7 +243,7 @@ struct Pnorm : KeyF64 {
       if constexpr (PK == 1) return acc + d;
       else if constexpr (PK == 3) return fma(d * d, d, acc);
       else if constexpr (PK == 4) { const double d2 = d * d; return fma(d2, d2, acc); }
-      else return acc + pow(d, p);
+      else return acc + pow_fast<PK>(d, p);
     }
   }
 };
@@ -441,6 +472,9 @@ constexpr const char* policy_name() {
   else if constexpr (std::is_same_v<P, Pnorm<3, false>>) return "Pnorm<3>";
   else if constexpr (std::is_same_v<P, Pnorm<4, false>>) return "Pnorm<4>";
   else if constexpr (std::is_same_v<P, Pnorm<0, false>>) return "Pnorm<p>";
+  else if constexpr (std::is_same_v<P, Pnorm<-3, false>>) return "Pnorm<1.5>";
+  else if constexpr (std::is_same_v<P, Pnorm<-5, false>>) return "Pnorm<2.5>";
+  else if constexpr (std::is_same_v<P, Pnorm<-7, false>>) return "Pnorm<3.5>";
   else if constexpr (std::is_same_v<P, Pnorm<1, true>>) return "Pnorm<1,exact>";
   else if constexpr (std::is_same_v<P, Pnorm<3, true>>) return "Pnorm<3,exact>";
   else if constexpr (std::is_same_v<P, Pnorm<4, true>>) return "Pnorm<4,exact>";
@@ -543,15 +577,11 @@ struct SweepParams {
   int k_hi;               // exclusive upper bound of the swept diagonal band
   int R;                  // rows per tile
   int row_hi;             // exclusive upper bound of the swept rows (L for a full sweep)
-  int rl;                 // index reflection: > 0 stores neighbour indices as rl - 1 - idx
-                          // (sweeps of the time-reversed series, used by the extension)
   double p;
   unsigned long long* stats;  // optional diagnostics (MPROF_STATS): [0] replays [1] offers
   double* scratch;            // L doubles of scratch (first-diagonal pass)
 };
 
-// Neighbour index as stored in the profile (original coordinates).
-__device__ __forceinline__ int out_index(int idx, int rl) { return rl > 0 ? rl - 1 - idx : idx; }
 
 template <class P>
 __device__ __forceinline__ const typename P::V2* pairs_of(const SweepParams& prm) {
@@ -604,15 +634,15 @@ struct Acc {
 // Positions (row, j) index the profile being swept; the stored neighbour indices are mapped by
 // out_index (identity except for reflected sweeps) so ties compare in original coordinates.
 __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhit, int row, int j,
-                                        int rl, int* ct, BestEntry* best, unsigned long long* rv,
+                                        int* ct, BestEntry* best, unsigned long long* rv,
                                         int* rj, unsigned long long* stats) {
   // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
   const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
   if (colhit) {
-    atomicMin(ct, static_cast<int>(offer(best, j, vb, out_index(row, rl)) >> 32));
+    atomicMin(ct, static_cast<int>(offer(best, j, vb, row) >> 32));
     if (stats) atomicAdd(&stats[1], 1ull);
   }
-  const int jo = out_index(j, rl);
+  const int jo = j;
   if (rowhit && lex_less(vb, jo, *rv, *rj)) {
     *rv = vb;
     *rj = jo;
@@ -627,7 +657,7 @@ __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhi
 // (u, d) uses run entry u + d.
 template <class P, int D, bool GUARD>
 __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, int i0, int kt, int kend,
-                                          int L, int rl, double p, const typename P::V2* cA1,
+                                          int L, double p, const typename P::V2* cA1,
                                           const typename P::V2* cA2, const typename P::VB* cB1,
                                           const typename P::VB* cB2, int* cT1, int* cT2,
                                           const typename P::V2* rowA, const typename P::VB* rowB,
@@ -635,7 +665,10 @@ __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, in
   using V2 = typename P::V2;
   using VB = typename P::VB;
   if (stats) atomicAdd(&stats[0], 1ull);
-#pragma unroll
+  // The row loop is rolled: a replay is the rare path, and its code must stay small -- on series
+  // where most blocks replay (noise-like data: loose thresholds everywhere) an unrolled 64-cell
+  // body thrashed the instruction cache (ncu: 61 % of stall samples "no instruction").
+#pragma unroll kReplayUnroll
   for (int u = 0; u < D; ++u) {
     if (GUARD && s + u >= cnt) break;
     const int x = s + u;
@@ -657,7 +690,7 @@ __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, in
       int* ct = e < D ? &cT1[e] : &cT2[e - D];
       const bool rowhit = h <= tr;
       const bool colhit = h <= *reinterpret_cast<volatile int*>(ct);
-      if (rowhit || colhit) merge_cell(v, h, rowhit, colhit, row, row + kt + d, rl, ct, best, &rv, &rj, stats);
+      if (rowhit || colhit) merge_cell(v, h, rowhit, colhit, row, row + kt + d, ct, best, &rv, &rj, stats);
     }
     if (rj != INT_MAX) {
       atomicMin(&rowT[x], static_cast<int>(offer(best, row, rv, rj) >> 32));
@@ -676,7 +709,7 @@ __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, in
 // cells of a sub-step are merged does not change the result. Called convergently by the warp.
 template <class P, int D, int HG, bool GUARD>
 __device__ __noinline__ void coop_replay(typename P::V a, int src, int s0, int cnt, int i0, int kts,
-                                         int kend, int L, int rl, double p,
+                                         int kend, int L, double p,
                                          const typename P::V2* colA, const typename P::VB* colB,
                                          int* colT, int X0, int xbs, int ring,
                                          const typename P::V2* rowA, const typename P::VB* rowB,
@@ -717,12 +750,12 @@ __device__ __noinline__ void coop_replay(typename P::V a, int src, int s0, int c
         const int tr = *reinterpret_cast<volatile int*>(&rowT[x]);
         const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
         if (h <= *reinterpret_cast<volatile int*>(ct)) {
-          atomicMin(ct, static_cast<int>(offer(best, j, vb, out_index(row, rl)) >> 32));
+          atomicMin(ct, static_cast<int>(offer(best, j, vb, row) >> 32));
           if (stats) atomicAdd(&stats[1], 1ull);
         }
         if (h <= tr) {
           rv = vb;
-          rj = out_index(j, rl);
+          rj = j;
         }
       }
 #pragma unroll
@@ -745,7 +778,7 @@ __device__ __noinline__ void coop_replay(typename P::V a, int src, int s0, int c
 // Merge of the seed cells (every valid cell, all lanes on the same row): columns per cell, the
 // row through a warp lexicographic reduction and one CAS per warp. Called convergently.
 template <int D>
-__device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, int col0, int rl,
+__device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, int col0,
                                           BestEntry* best) {
   unsigned long long rv = kInfBits;
   int rj = INT_MAX;
@@ -755,8 +788,8 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
     const double v = c.v[d];
     const unsigned long long vb = (__double2hiint(v) < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
     const int j = col0 + d;
-    offer(best, j, vb, out_index(row, rl));
-    const int jo = out_index(j, rl);
+    offer(best, j, vb, row);
+    const int jo = j;
     if (lex_less(vb, jo, rv, rj)) {
       rv = vb;
       rj = jo;
@@ -813,6 +846,9 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #ifndef MPROF_HIT_VOTE
 #define MPROF_HIT_VOTE 0
 #endif
+#ifndef MPROF_SPLIT_DFMA
+#define MPROF_SPLIT_DFMA 0
+#endif
 #ifndef MPROF_HIT_GROUP_DS
 #define MPROF_HIT_GROUP_DS 2    // (delta, sigma) AAMP, FP64 and FP32
 #endif
@@ -835,7 +871,7 @@ __host__ __device__ constexpr int hit_group_for() {
 template <class P, int D, int T, int S, bool GUARD>
 __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int X0,
                                           typename P::V (&acc)[D], int i0, int cnt, int kt,
-                                          int kend, int L, int rl, BestEntry* best, double p,
+                                          int kend, int L, BestEntry* best, double p,
                                           unsigned long long* stats) {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
@@ -928,9 +964,23 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
         const V2 r = rowA[x];
         const int row = i0 + x + 1;
         int hu = ZQ ? INT_MIN : INT_MAX;
+#if MPROF_SPLIT_DFMA
+        if constexpr (P::kCovFilter && sizeof(typename P::V) == 8) {
+          // the two DFMAs of the slide as two passes over the D diagonals: each pass reads the
+          // same row operand in the same slot (register reuse cache), same arithmetic as step()
+          typename P::V tmp[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) tmp[d] = fma(cA[(d + u) % D].x, r.y, acc[d]);
+#pragma unroll
+          for (int d = 0; d < D; ++d) acc[d] = fma(cA[(d + u) % D].y, r.x, tmp[d]);
+        }
+#endif
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           const int sl = (d + u) % D;
+#if MPROF_SPLIT_DFMA
+          if constexpr (!(P::kCovFilter && sizeof(typename P::V) == 8))
+#endif
           acc[d] = P::step(acc[d], r, cA[sl], p);
           if constexpr (ZQ) {
             if (!SKON || (u & 1)) {
@@ -976,7 +1026,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
           const typename P::V v = __shfl_sync(0xffffffffu, acc0.a[d], src);
           if (lane == d) a = v;
         }
-        coop_replay<P, D, HG, GUARD>(a, src, s0, cnt, i0, kt + (src - lane) * D, kend, L, rl, p,
+        coop_replay<P, D, HG, GUARD>(a, src, s0, cnt, i0, kt + (src - lane) * D, kend, L, p,
                                      sm.colA, sm.colB, sm.colT[b], X0, (threadIdx.x - lane + src) * D,
                                      G::RING, rowA, sm.rowB[b], sm.rowT[b], best, stats);
       }
@@ -997,7 +1047,7 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
         if (HG > 1 && GUARD && s >= cnt) break;
         const int q1 = G::pad((X0 + s + xb) % G::RING);
         const int q2 = G::pad((X0 + s + xb + D) % G::RING);
-        acc0 = replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, rl, p, &sm.colA[q1],
+        acc0 = replay_block<P, D, GUARD>(acc0, s, cnt, i0, kt, kend, L, p, &sm.colA[q1],
                                          &sm.colA[q2], &sm.colB[P::kHasB ? q1 : 0],
                                          &sm.colB[P::kHasB ? q2 : 0], &colT[G::pad(s + xb)],
                                          &colT[G::pad(s + xb + D)], rowA, sm.rowB[b], sm.rowT[b],
@@ -1254,7 +1304,7 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   const int L = prm.L;
   const int m = prm.m;
   const int kt = kb + static_cast<int>(threadIdx.x) * D;
-  const int kend = min(kb + G::K, prm.k_hi);
+  const int kend = min(min(tl.w, kb + G::K), prm.k_hi);  // the tile's diagonals: [kb, kend)
   if constexpr (is_euclid_cov<P>()) {
     if (threadIdx.x == 0) g_cell_ctx = CellCtx{prm.S, prm.mu, static_cast<double>(m)};
     __syncthreads();
@@ -1326,7 +1376,7 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
       c.v[d] = ok ? cell_value<P>(acc[d], rb, cb, ra, ra + k) : 0.0;
       valid |= (ok ? 1u : 0u) << d;
     }
-    resolve_seed<D>(c, valid, ra, ra + kt, prm.rl, prm.best);
+    resolve_seed<D>(c, valid, ra, ra + kt, prm.best);
   }
 
   // ---- stage pipeline over the row transitions ra .. re-2 ---------------------------------
@@ -1350,11 +1400,11 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
     const int s0 = st * S;
     const int cnt = min(S, steps - s0);
     const int i0 = ra + s0;
-    const bool full = (cnt == S) && (kb + G::K <= prm.k_hi) && (i0 + cnt + kb + G::K - 1 <= L - 1);
+    const bool full = (cnt == S) && (kb + G::K <= kend) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {
-      run_stage<P, D, T, S, false>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.rl, prm.best, prm.p, prm.stats);
+      run_stage<P, D, T, S, false>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     } else {
-      run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.rl, prm.best, prm.p, prm.stats);
+      run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     }
     if (st + 1 == nst) break;
     cp_async_wait<0>();

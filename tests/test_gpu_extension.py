@@ -1,8 +1,11 @@
 """Streaming extension: build_engine_state / extend_profile. The reference's
 acceptance criterion 7 (/root/reference/proj/tests/acceptance.cpp:252-286): 50 rounds of
 random series, a build over the first n0 samples, an extension by 1..40 samples, compared with a
-from-scratch run of the whole series (there with 1e-9 and identical indices; here with the GPU
-parity rules — the GPU re-derives the new cells, it does not replay the CPU cursors)."""
+from-scratch run of the whole series (1e-9 and identical indices there). The GPU extension plans
+the extended series as a fresh build would and sweeps only the fresh sweep's tiles that hold new
+cells (the stored entries seed the rest), so the grown profile is BIT-IDENTICAL to a fresh GPU
+profile of the extended series (tests/test_engine_state.cpp:31-37 checks it with ==), and within
+the parity rules of the oracle."""
 import numpy as np
 import pytest
 
@@ -101,3 +104,72 @@ def test_extension_exact_and_fp32_modes(mp):
         _, P64, _ = oracle.scan(t, m, fam, p)
         excess = (st.profile.distances - P64) / np.maximum(1, P64)
         assert excess.max() <= (5e-3 if fam == ZNORM else 1e-4), excess.max()
+
+
+def fresh(mp, t, cfg):
+    fam = cfg.kind.family
+    ts = mp.make_time_series(t)
+    if fam == mp.DistanceFamily.Euclidean:
+        return mp.aamp(ts, cfg)
+    if fam == mp.DistanceFamily.PNorm:
+        return mp.aamp_pnorm(ts, cfg)
+    return mp.acamp(ts, cfg)
+
+
+def test_extension_bit_identical_to_fresh(mp):
+    """The reference's own contract (test_engine_state.cpp "many random build-then-extend cases
+    match from scratch", acceptance criterion 7): exact equality, ties included (short z-normalized
+    windows of uniform noise tie exactly)."""
+    r = np.random.default_rng(702)
+    fams = [(EUCLIDEAN, 2.0), (PNORM, 2.5), (ZNORM, 2.0), (PNORM, 1.0)]
+    for rnd in range(60):
+        n0 = int(24 + r.integers(0, 80))
+        extra = int(1 + r.integers(0, 40))
+        m = int(2 + r.integers(0, n0 // 2))
+        allv = r.uniform(-1, 1, n0 + extra) if rnd % 2 == 0 else r.standard_normal(n0 + extra)
+        fam, p = fams[rnd % 4]
+        cfg = mp.ProfileConfig(m, kind(mp, fam, p))
+        st = mp.build_engine_state(mp.make_time_series(allv[:n0]), cfg)
+        grown = mp.extend_profile(st, allv[n0:])
+        want = fresh(mp, allv, cfg)
+        assert np.array_equal(grown.profile.nn_index, want.nn_index), rnd
+        assert np.array_equal(grown.profile.distances, want.distances), rnd
+
+
+@pytest.mark.parametrize("fam,p", [(EUCLIDEAN, 2.0), (ZNORM, 2.0)])
+def test_large_extension_incremental_and_bit_identical(mp, fam, p):
+    """A C4-prefix series grown by 2 000 samples: only the tiles holding new windows run (fewer
+    cells than a fresh sweep) and the result equals the fresh profile bit for bit. (The rows per
+    tile are planned on the profile length rounded up to 1/8 of its octave: both lengths here
+    plan alike, so the extension is incremental.)"""
+    from paper_1901_05708_b200 import workloads as W
+    t = W.c4()[: (1 << 18) - 1000]
+    cfg = mp.ProfileConfig(1024, kind(mp, fam, p))
+    st = mp.build_engine_state(mp.make_time_series(t[:-2000]), cfg)
+    grown = mp.extend_profile(st, t[-2000:])
+    want = fresh(mp, t, cfg)
+    assert grown.info.cells < 0.5 * want.info.cells, (grown.info.cells, want.info.cells)
+    assert np.array_equal(grown.profile.nn_index, want.nn_index)
+    assert np.array_equal(grown.profile.distances, want.distances)
+
+
+def test_cancelled_build_is_incomplete(mp):
+    """tests/test_engine_state.cpp:128-137: a build cancelled by its observer is incomplete, keeps
+    the completed diagonals (ascending from the exclusion) and cannot be extended."""
+    r = np.random.default_rng(703)
+    t = r.uniform(-1, 1, 64)
+    cfg = mp.ProfileConfig(6, mp.DistanceKind.euclidean())
+    st = mp.build_engine_state(mp.make_time_series(t), cfg, progress=lambda d, n: d < 10)
+    assert not st.complete()
+    assert list(st.completed_diagonals) == list(range(1, 11))
+    assert st.tail().shape == (10,)
+    with pytest.raises(mp.Error) as e:
+        mp.extend_profile(st, [0.5])
+    assert e.value.code == mp.ErrorCode.IncompleteState
+    full = mp.build_engine_state(mp.make_time_series(t), cfg)
+    assert full.complete() and len(full.completed_diagonals) == 64 - 6
+    # tail cursors: the accumulator of each diagonal's last cell (pos = n - m - k)
+    tail = full.tail()
+    for k in (1, 7, 58):
+        pos = 64 - 6 - k
+        assert abs(tail[k - 1] - np.sum((t[pos:pos + 6] - t[pos + k:pos + k + 6]) ** 2)) < 1e-12
