@@ -53,8 +53,13 @@ def parse():
     ap.add_argument("--m", type=int, default=M_C4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config sweep timings of C1/C2/C3/C5 and C4 FP32")
     ap.add_argument("--merge", choices=["peer", "nccl"], default="peer",
                     help="N > 1: fused peer-memory merge (default) or the two-ncclMin baseline")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="tests only: every rank on cuda:0, gloo + host barriers (NCCL cannot run "
+                         "two ranks on one GPU); exercises the N > 1 path on a one-GPU box")
     return ap.parse_args()
 
 
@@ -127,6 +132,16 @@ class Clocks:
 # ------------------------------------------------------------------------------------------------
 # CPU baseline: the reference's own implementation on the host cores (bounded sample)
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(t, m, engines, threads=None):
     import oracle
     threads = threads or (os.cpu_count() or 1)
@@ -143,6 +158,9 @@ def cpu_baseline(t, m, engines, threads=None):
         total_s += time.perf_counter() - t0
         total_cells += cells(sample.size, m)
     return {"value": total_cells / total_s, "unit": UNIT, "cores": threads, "kind": kind,
+            "cpu": cpu_model(),
+            "full_c4_record": "profiles/r02_cpu_reference_c4.json (one-off full-C4 timing of the "
+                              "reference on this pool's host cores, threads = all and 1)",
             "sample": f"{'+'.join(engines)} on the first {sample.size} samples of the same series, "
                       f"m={m} ({total_cells:.3e} cells, {total_s:.2f} s wall, "
                       f"{'oracle/_ref = reference C++ built -O3' if kind == 'reference' else 'oracle C restatement'})"}
@@ -216,9 +234,15 @@ def main():
                                                    merge_min_, shard_size)
 
     rank, world, local = env_rank()
+    share = args.share_gpu and world > 1
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, m = args.n, args.m
     L = n - m + 1
     engines = args.engines.split(",")
@@ -242,13 +266,19 @@ def main():
     # N > 1: the fused peer-memory merge (one kernel per rank over CUDA-IPC / NVLink buffers,
     # stream-ordered NCCL one-word barriers) unless --merge nccl asks for the ncclMin baseline
     peers = {}
-    if world > 1 and args.merge == "peer":
+    if world > 1 and (args.merge == "peer" or share):
         try:
-            peers = {e: PeerExchange(mp, L, ctx=ctx, barrier="nccl") for e in engines}
+            peers = {e: PeerExchange(mp, L, ctx=ctx, barrier="host" if share else "nccl")
+                     for e in engines}
         except Exception as ex:  # no IPC / peer access: the ncclMin path still works
+            if share:
+                raise
             print(f"[bench] peer merge unavailable ({ex}); using the ncclMin merge", file=sys.stderr)
             peers = {}
 
+    # planned sweeps: the per-series decisions (form probe, rows per tile, tile tables) are taken
+    # once here; each step only enqueues kernels (mprof_plan_sweep)
+    plans = {e: mp.Plan(d_t.data_ptr(), n, cfgs[e], band[0], band[1], ctx=ctx) for e in engines}
     sweep_ms = {e: [] for e in engines}
     ops_per_cell = {}
     launches = [0]
@@ -260,17 +290,14 @@ def main():
                 cmp, idx, P = bufs[e]
                 if e in peers:
                     px = peers[e]
-                    info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1], px.cmp,
-                                           px.idx, ctx=ctx)
+                    info = plans[e].sweep(px.cmp, px.idx)
                     px.merge_finalize(d_t.data_ptr(), n, cfgs[e])
                 elif world > 1:
-                    info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1],
-                                           cmp.data_ptr(), idx.data_ptr(), ctx=ctx)
+                    info = plans[e].sweep(cmp.data_ptr(), idx.data_ptr())
                     merge_min_(cmp, idx)
                     finalize_sharded(mp, d_t.data_ptr(), n, cmp, idx, cfgs[e], P, ctx=ctx)
                 else:
-                    info = mp.sweep_device(d_t.data_ptr(), n, cfgs[e], band[0], band[1],
-                                           cmp.data_ptr(), idx.data_ptr(), ctx=ctx)
+                    info = plans[e].sweep(cmp.data_ptr(), idx.data_ptr())
                     mp.finalize_device(d_t.data_ptr(), n, cmp.data_ptr(), idx.data_ptr(), cfgs[e],
                                        P.data_ptr(), ctx=ctx)
                 if record:
@@ -301,7 +328,7 @@ def main():
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        x = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        x = torch.tensor([ms], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         ms = float(x.item())
     total_cells = cells(n, m) * len(engines)
@@ -348,11 +375,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": {"workload": f"C4 {'+'.join(engines)}: n={n}, m={m}, exclusion 1, FP64, "
+                                   f"{'(ranks sharing cuda:0, test mode) ' if share else ''}"
                                    f"{('equal-area diagonal bands + fused peer-memory merge/finalize' if peers else 'equal-area diagonal bands + ncclMin merge + sharded finalize') if world > 1 else 'single GPU'}",
                        "n": n, "m": m, "engines": engines, "cells_per_step": total_cells,
                        "l2": "flushed every step (256 MiB memset inside the timed region)",
                        "parallelism": f"diagonal-band dp{world}"},
             "roofline": roofline, "gpu_launches": launches[0], "clocks": clk}
+
+    # the other BASELINE.json configurations (1 GPU): sweep-kernel times of each engine, so the
+    # driver sees every config's rate next to the headline (C4 FP64 above)
+    if world == 1 and not args.no_configs:
+        line["configs"] = other_configs(mp, ctx, peak_gflops)
 
     # end to end through the public API: pinned host series in, P and I back to the host
     if not args.no_e2e:
@@ -364,6 +397,41 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_configs(mp, ctx, peak_gflops):
+    """Sweep time (CUDA events on the launching stream, best of the timed repeats after one
+    warm-up) of every BASELINE.json configuration other than the headline: C1 AAMP, C2 ACAMP,
+    C3 p-norm p = 1 and 3, C5 ACAMP (FP64) and C4 AAMP / ACAMP in FP32 mode. frac_of_fp64_peak
+    counts SURVEY.md 8(d)'s algorithmic flops per cell against the live FP64 peak (FP32 rows:
+    informational, same formula)."""
+    from paper_1901_05708_b200 import workloads as W
+    cases = [("C1 AAMP n=2^14 m=100", W.c1, 100, mp.DistanceKind.euclidean(), mp.Precision.FP64, "aamp", 3),
+             ("C2 ACAMP n=2^17 m=256", W.c2, 256, mp.DistanceKind.znormalized(), mp.Precision.FP64, "acamp", 3),
+             ("C3 p-norm p=1 n=2^18 m=128", W.c3, 128, mp.DistanceKind.pnorm(1.0), mp.Precision.FP64, "pnorm1", 3),
+             ("C3 p-norm p=3 n=2^18 m=128", W.c3, 128, mp.DistanceKind.pnorm(3.0), mp.Precision.FP64, "pnorm3", 3),
+             ("C5 ACAMP n=2^22 m=512", W.c5, 512, mp.DistanceKind.znormalized(), mp.Precision.FP64, "acamp", 1),
+             ("C4 AAMP FP32 n=2^20 m=1024", W.c4, 1024, mp.DistanceKind.euclidean(), mp.Precision.FP32, "aamp", 2),
+             ("C4 ACAMP FP32 n=2^20 m=1024", W.c4, 1024, mp.DistanceKind.znormalized(), mp.Precision.FP32, "acamp", 2)]
+    out = {}
+    series = {}
+    for name, gen, m, kind, prec, fl, reps in cases:
+        if gen not in series:
+            series[gen] = mp.make_time_series(gen())
+        cfg = mp.ProfileConfig(m, kind)
+        cfg.precision = prec
+        fn = {mp.DistanceFamily.Euclidean: mp.aamp, mp.DistanceFamily.PNorm: mp.aamp_pnorm,
+              mp.DistanceFamily.ZNormalized: mp.acamp}[kind.family]
+        fn(series[gen], cfg, ctx=ctx)
+        best = None
+        for _ in range(reps):
+            r = fn(series[gen], cfg, ctx=ctx)
+            best = r.info.sweep_ms if best is None else min(best, r.info.sweep_ms)
+        cps = r.info.cells / (best * 1e-3)
+        out[name] = {"sweep_ms": round(best, 4), "cells_per_s": cps, "policy": r.info.policy,
+                     "precision": prec.name,
+                     "frac_of_fp64_peak": cps * FLOPS_PER_CELL[fl] / (peak_gflops * 1e9)}
+    return out
 
 
 def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, peers, stream):
@@ -421,7 +489,7 @@ def e2e(args, mp, torch, dist, t, n, m, engines, cfgs, band, world, rank, ctx, p
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     if world > 1:
-        x = torch.tensor([el], dtype=torch.float64, device="cuda")
+        x = torch.tensor([el], dtype=torch.float64, device="cpu" if args.share_gpu else "cuda")
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         el = float(x.item())
     total = cells(n, m) * len(engines) * args.steps

@@ -179,6 +179,19 @@ int32_t mprof_brute_rows(mprof_ctx* ctx, const double* t, uint64_t n, const mpro
 int32_t mprof_sweep_device(mprof_ctx* ctx, const double* d_t, uint64_t n, const mprof_config* cfg,
                            uint64_t k_lo, uint64_t k_hi, double* d_cmp, int64_t* d_idx,
                            mprof_run_info* info);
+/* Planned band sweeps: mprof_plan_create takes every per-series decision of the sweep of band
+ * [k_lo, k_hi) (0, 0 = all) of series d_t ONCE, synchronously -- operand statistics, the filter
+ * form (spread test, form probe), rows per tile, the band's tile table -- into a plan that owns
+ * its workspace; mprof_plan_sweep then only enqueues kernels on the context's stream (no host
+ * synchronisation unless the context times the sweep), so repeated sweeps of a fixed series can
+ * be captured in a CUDA graph. Results are identical to mprof_sweep_device's. The series must not
+ * change while the plan is used; one plan must not be swept concurrently from two threads. */
+typedef struct mprof_plan mprof_plan;
+int32_t mprof_plan_create(mprof_ctx* ctx, const double* d_t, uint64_t n, const mprof_config* cfg,
+                          uint64_t k_lo, uint64_t k_hi, mprof_plan** out);
+int32_t mprof_plan_sweep(mprof_plan* plan, double* d_cmp, int64_t* d_idx, mprof_run_info* info);
+void mprof_plan_destroy(mprof_plan* plan);
+
 /* Distances d_P[L] of a (merged) comparison-space profile of series d_t (n samples), the
  * finalization of run_engine (to_distance / f_to_dz, /root/reference/proj/src/detail/diag_scan.hpp:
  * 153-167). Default mode: the distance of each chosen pair (i, d_idx[i]) is recomputed directly
@@ -264,11 +277,13 @@ void mprof_state_destroy(mprof_state* st);
 /* ---- one process, several GPUs ------------------------------------------------------------ */
 /* The entry points above on `ndev` devices: the admissible diagonals are split into equal-area
  * bands (mprof_band_cuts), device devices[g] sweeps band g from its own host thread and context,
- * the partial profiles are merged on devices[0] (peer copies over NVLink + the lexicographic
- * merge kernel, = MinBuffer::absorb, /root/reference/proj/src/detail/diag_scan.hpp:45-52) and
- * finalized there. engine: 0 = mprof_aamp, 1 = mprof_aamp_pnorm, 2 = mprof_acamp (same
+ * the partial profiles are merged on devices[0] (the lexicographic merge = MinBuffer::absorb,
+ * /root/reference/proj/src/detail/diag_scan.hpp:45-52) and finalized there. engine: 0 =
+ * mprof_aamp, 1 = mprof_aamp_pnorm, 2 = mprof_acamp (same
  * validation and BadKind rule; both AcampVariants give the same profile). A device may be listed
- * more than once. This replaces the reference's `threads` worker split
+ * more than once (at most MPROF_MAX_PEERS entries). The partials are merged and finalized by one
+ * kernel on devices[0] that reads them over NVLink peer access (copies where peer access is
+ * unavailable). This replaces the reference's `threads` worker split
  * (/root/reference/proj/src/detail/diag_scan.hpp:228-256) with a device split; progress
  * observers are not called. */
 int32_t mprof_profile_multi(const int32_t* devices, uint32_t ndev, int32_t engine, const double* t,

@@ -32,7 +32,7 @@ __all__ = [
     "aamp_pnorm", "acamp", "sweep_device", "finalize_device", "merge_device", "band_cuts",
     "band_cells", "fp64_peak", "lib", "LIB_PATH", "Context", "EngineState",
     "build_engine_state", "extend_profile", "brute_profile", "ipc_alloc", "ipc_free",
-    "ipc_open", "ipc_close", "merge_finalize_peers",
+    "ipc_open", "ipc_close", "merge_finalize_peers", "Plan",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libmprof_gpu.so"
@@ -279,6 +279,10 @@ EXPORTS = {
     "mprof_state_tail": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "mprof_ctx_set_progress": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "mprof_ctx_set_form": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "mprof_plan_create": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
+                                      C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "mprof_plan_sweep": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(RunInfo)]),
+    "mprof_plan_destroy": (None, [C.c_void_p]),
     "mprof_brute_profile": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
                                         C.c_void_p, C.c_void_p]),
     "mprof_brute_rows": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
@@ -494,6 +498,36 @@ def sweep_device(d_t: int, n: int, cfg: ProfileConfig, k_lo: int, k_hi: int, d_c
     _raise(lib().mprof_sweep_device(_ctx_handle(ctx), C.c_void_p(d_t), n, C.byref(c), k_lo, k_hi,
                                     C.c_void_p(d_cmp), C.c_void_p(d_idx), C.byref(info)))
     return info
+
+
+class Plan:
+    """A planned band sweep of one device-resident series (mprof_plan_create): the per-series
+    decisions are taken once; sweep() only enqueues kernels (no host synchronisation)."""
+
+    def __init__(self, d_t: int, n: int, cfg: ProfileConfig, k_lo: int = 0, k_hi: int = 0,
+                 ctx: Optional[Context] = None):
+        self.cfg = cfg
+        self._c = _to_c(cfg)
+        h = C.c_void_p()
+        _raise(lib().mprof_plan_create(_ctx_handle(ctx), C.c_void_p(d_t), n, C.byref(self._c),
+                                       k_lo, k_hi, C.byref(h)))
+        self.handle = h
+
+    def sweep(self, d_cmp: int, d_idx: int) -> RunInfo:
+        info = RunInfo()
+        _raise(lib().mprof_plan_sweep(self.handle, C.c_void_p(d_cmp), C.c_void_p(d_idx), C.byref(info)))
+        return info
+
+    def close(self) -> None:
+        if self.handle:
+            lib().mprof_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def finalize_device(d_t: int, n: int, d_cmp: int, d_idx: int, cfg: ProfileConfig, d_P: int,

@@ -62,10 +62,15 @@ constexpr double kProbeMaxReplays = 5e-6, kProbeMinCells = 4e9;
 // walk m = 512 1.6e-5; where the column-scaled form wins: C3 sinusoids m = 1024 4.7e-5, m = 256
 // 7.1e-4.
 constexpr double kProbeMaxReplaysZ = 3e-5;
-// Longer hit groups (Wide<P>) when the probe saw at most ~2 replays in its 3.9e7 cells: measured
+// Longer hit groups (Wide<P>) when the probe saw at most 1e-5 replayed blocks per cell: measured
 // HG 2 -> 4, C4 AAMP 115.7 -> 113.2 ms, C4 ACAMP 116.6 -> 115.2 ms (0 probe replays), while a
-// random walk m = 256 AAMP (10 probe replays) went 8.11 -> 8.27 and C5 (834) 2054 -> 2365.
-constexpr double kProbeWideMaxReplays = 5e-8;
+// random walk m = 256 AAMP (10 probe replays) went 8.11 -> 8.27 and C5 (834) 2054 -> 2365. The
+// bound was 5e-8 (~2 replays) in round 1; the round-2 probe sample sees 204 replays on C4 ACAMP
+// (5.3e-6 per cell), where HG 8 still measured 118.7 -> 115.9 ms; C5 (2e-5) keeps HG 2.
+#ifndef MPROF_WIDE_MAX_REPLAYS
+#define MPROF_WIDE_MAX_REPLAYS 1e-5
+#endif
+constexpr double kProbeWideMaxReplays = MPROF_WIDE_MAX_REPLAYS;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
@@ -827,6 +832,22 @@ struct mprof_state {
   int plan_flags = 0;
 };
 
+// A planned band sweep of one series (mprof_plan_create): the per-series decisions, the prepared
+// operands and the band's tile table, so that mprof_plan_sweep only enqueues kernels.
+struct mprof_plan {
+  mprof_ctx* ctx = nullptr;  // borrowed
+  const double* t = nullptr;
+  uint64_t n = 0;
+  mprof_config cfg;
+  long long k_lo = 0, k_hi = 0;  // admissible band
+  void* ws = nullptr;            // owned workspace (operands, profile, scratch)
+  int4* tiles = nullptr;         // owned tile table
+  long long ntiles = 0, n_near = 0, R = 0;
+  bool aamp_cov = false, zn_colscale = false, wide = false;
+  unsigned long long probe_replays = 0;
+  double probe_cells = 0.0;
+};
+
 namespace {
 
 int32_t ensure(void** p, size_t* have, size_t need) {
@@ -919,7 +940,7 @@ struct Workspace {
   float2* SB;       // ring scalars {S rd, mu - t[0] rd}
 };
 
-int32_t carve(mprof_ctx* c, int L, Workspace* w) {
+size_t workspace_bytes(int L) {
   const size_t nA = align_up(sizeof(double2) * (size_t)L);
   const size_t nB = align_up(sizeof(double) * (size_t)L);
   const size_t nBest = align_up(sizeof(BestEntry) * (size_t)L);
@@ -927,10 +948,18 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   const size_t nA32 = align_up(sizeof(float2) * (size_t)L);
   const size_t nB32 = align_up(sizeof(float) * (size_t)L);
   const size_t nS = align_up(8 * sizeof(double));
-  const int32_t st = ensure(&c->ws, &c->ws_bytes,
-                            nA + 3 * nB + nBest + nC + nA32 + nB32 + nS + nA + 2 * nB + nA32);
-  if (st != MPROF_OK) return st;
-  char* base = static_cast<char*>(c->ws);
+  return nA + 3 * nB + nBest + nC + nA32 + nB32 + nS + nA + 2 * nB + nA32;
+}
+
+// The workspace arrays of a profile of length L laid out from `base` (workspace_bytes(L) bytes).
+void carve_at(char* base, int L, Workspace* w) {
+  const size_t nA = align_up(sizeof(double2) * (size_t)L);
+  const size_t nB = align_up(sizeof(double) * (size_t)L);
+  const size_t nBest = align_up(sizeof(BestEntry) * (size_t)L);
+  const size_t nC = align_up(sizeof(int) * ((size_t)L / kChunk + 2));
+  const size_t nA32 = align_up(sizeof(float2) * (size_t)L);
+  const size_t nB32 = align_up(sizeof(float) * (size_t)L);
+  const size_t nS = align_up(8 * sizeof(double));
   w->A = reinterpret_cast<double2*>(base);
   w->B = reinterpret_cast<double*>(base + nA);
   w->mu = reinterpret_cast<double*>(base + nA + nB);
@@ -945,6 +974,13 @@ int32_t carve(mprof_ctx* c, int L, Workspace* w) {
   w->emu = reinterpret_cast<double*>(e + nA);
   w->S = reinterpret_cast<double*>(e + nA + nB);
   w->SB = reinterpret_cast<float2*>(e + nA + 2 * nB);
+}
+
+// The context's grow-only workspace, carved for a profile of length L.
+int32_t carve(mprof_ctx* c, int L, Workspace* w) {
+  const int32_t st = ensure(&c->ws, &c->ws_bytes, workspace_bytes(L));
+  if (st != MPROF_OK) return st;
+  carve_at(static_cast<char*>(c->ws), L, w);
   return MPROF_OK;
 }
 
@@ -2106,6 +2142,7 @@ int32_t mprof_profile_multi(const int32_t* devices, uint32_t ndev, int32_t engin
                             mprof_run_info* info) {
   if (!devices || ndev == 0 || !t || !cfg || !P || !I) return fail(MPROF_E_BAD_ARG, "null argument");
   if (engine < 0 || engine > 2) return fail(MPROF_E_BAD_ARG, "unknown engine %d", engine);
+  if (ndev > MPROF_MAX_PEERS) return fail(MPROF_E_BAD_ARG, "at most %d bands (devices listed)", MPROF_MAX_PEERS);
   int32_t st = check_series(t, n);
   if (st != MPROF_OK) return st;
   st = check_config(n, cfg);
@@ -2187,40 +2224,59 @@ int32_t mprof_profile_multi(const int32_t* devices, uint32_t ndev, int32_t engin
       cudaSetDevice(caller_dev);
       return s;
     }
-  // merge the partial profiles on the first device (peer copies over NVLink, then the
-  // lexicographic MinBuffer::absorb kernel), finalize there
+  // merge + finalize on the first device in ONE kernel that reads every band's partial (cmp, idx)
+  // in place over NVLink peer access (k_merge_finalize_peers, MinBuffer::absorb + finalize, the
+  // same kernel the multi-process path uses); without peer access between two of the devices the
+  // partials are first copied to the first device (cudaMemcpyPeer) and merged from there
   Part& p0 = parts[0];
   mprof_ctx* c0 = p0.ctx;
   auto finish = [&]() -> int32_t {
     CK(cudaSetDevice(p0.dev));
-    double* s_cmp = nullptr;
-    int64_t* s_idx = nullptr;
-    double* d_P = nullptr;
-    CK(cudaMalloc(&d_P, L * sizeof(double)));
-    if (ndev > 1) {
-      CK(cudaMalloc(&s_cmp, L * sizeof(double)));
-      CK(cudaMalloc(&s_idx, L * sizeof(int64_t)));
-    }
+    std::vector<void*> owned;  // device-0 copies of partials without peer access, d_P, d_I
+    auto dev_alloc = [&](size_t bytes) -> void* {
+      void* q = nullptr;
+      if (cudaMalloc(&q, bytes) != cudaSuccess) return nullptr;
+      owned.push_back(q);
+      return q;
+    };
+    std::vector<const double*> in_cmp(ndev);
+    std::vector<const int64_t*> in_idx(ndev);
     int32_t s = MPROF_OK;
-    for (uint32_t g = 1; g < ndev && s == MPROF_OK; ++g) {
+    for (uint32_t g = 0; g < ndev && s == MPROF_OK; ++g) {
       const Part& q = parts[g];
-      if (q.dev != p0.dev) {
+      in_cmp[g] = q.d_cmp;
+      in_idx[g] = q.d_idx;
+      if (q.dev == p0.dev) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, p0.dev, q.dev);
+      if (can) {
         const cudaError_t e = cudaDeviceEnablePeerAccess(q.dev, 0);
-        if (e != cudaSuccess) cudaGetLastError();  // already enabled / no P2P: copies still work
+        if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          continue;
+        }
+        cudaGetLastError();
       }
-      CK(cudaMemcpyPeerAsync(s_cmp, p0.dev, q.d_cmp, q.dev, L * sizeof(double), c0->stream));
-      CK(cudaMemcpyPeerAsync(s_idx, p0.dev, q.d_idx, q.dev, L * sizeof(int64_t), c0->stream));
-      s = mprof_merge_device(c0, p0.d_cmp, p0.d_idx, s_cmp, s_idx, L);
+      double* cc = static_cast<double*>(dev_alloc(L * sizeof(double)));
+      int64_t* ci = static_cast<int64_t*>(dev_alloc(L * sizeof(int64_t)));
+      if (!cc || !ci) return fail(MPROF_E_OOM, "merge staging");
+      CK(cudaMemcpyPeerAsync(cc, p0.dev, q.d_cmp, q.dev, L * sizeof(double), c0->stream));
+      CK(cudaMemcpyPeerAsync(ci, p0.dev, q.d_idx, q.dev, L * sizeof(int64_t), c0->stream));
+      in_cmp[g] = cc;
+      in_idx[g] = ci;
     }
-    if (s == MPROF_OK) s = mprof_finalize_device(c0, p0.d_t, n, p0.d_cmp, p0.d_idx, cfg, d_P);
+    double* d_P = static_cast<double*>(dev_alloc(L * sizeof(double)));
+    int64_t* d_I = static_cast<int64_t*>(dev_alloc(L * sizeof(int64_t)));
+    if (!d_P || !d_I) s = fail(MPROF_E_OOM, "merge output");
+    if (s == MPROF_OK)
+      s = mprof_merge_finalize_peers(c0, p0.d_t, n, cfg, in_cmp.data(), in_idx.data(), ndev, &d_P,
+                                     &d_I, 1, 0, L);
     if (s == MPROF_OK) {
       CK(cudaMemcpyAsync(P, d_P, L * sizeof(double), cudaMemcpyDeviceToHost, c0->stream));
-      CK(cudaMemcpyAsync(I, p0.d_idx, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c0->stream));
+      CK(cudaMemcpyAsync(I, d_I, L * sizeof(int64_t), cudaMemcpyDeviceToHost, c0->stream));
       CK(cudaStreamSynchronize(c0->stream));
     }
-    cudaFree(d_P);
-    cudaFree(s_cmp);
-    cudaFree(s_idx);
+    for (void* q : owned) cudaFree(q);
     return s;
   };
   st = finish();
@@ -2237,7 +2293,7 @@ int32_t mprof_profile_multi(const int32_t* devices, uint32_t ndev, int32_t engin
       info->sweep_ms = std::max(info->sweep_ms, q.info.sweep_ms);
     }
     info->diagonals = L - cfg->exclusion;
-    info->kernel_launches += 2 * (ndev - 1) + 1;  // merges (+copies) and the finalize
+    info->kernel_launches += 1;  // the fused merge + finalize
   }
   const std::string keep = g_last_error;
   release();
@@ -2519,6 +2575,128 @@ int32_t mprof_ctx_set_progress(mprof_ctx* in, mprof_progress_fn fn, void* user) 
   if (st != MPROF_OK) return st;
   c->progress = fn;
   c->progress_user = user;
+  return MPROF_OK;
+}
+
+void mprof_plan_destroy(mprof_plan* P) {
+  if (!P) return;
+  if (P->ctx) {
+    cudaSetDevice(P->ctx->device);
+    cudaStreamSynchronize(P->ctx->stream);
+  }
+  cudaFree(P->ws);
+  cudaFree(P->tiles);
+  delete P;
+}
+
+int32_t mprof_plan_create(mprof_ctx* in, const double* d_t, uint64_t n64, const mprof_config* cfg,
+                          uint64_t k_lo64, uint64_t k_hi64, mprof_plan** out) {
+  if (!d_t || !cfg || !out) return fail(MPROF_E_BAD_ARG, "null argument");
+  *out = nullptr;
+  if (n64 < 2) return fail(MPROF_E_TOO_SHORT, "time series needs at least 2 samples");
+  int32_t st = check_config(n64, cfg);
+  if (st != MPROF_OK) return st;
+  if (cfg->precision == MPROF_FP32 && cfg->exact)
+    return fail(MPROF_E_BAD_ARG, "the exact (parity) mode is FP64 only");
+  mprof_ctx* c = nullptr;
+  st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  const int n = (int)n64, L = n - (int)cfg->m + 1;
+  mprof_plan* P = new mprof_plan();
+  P->ctx = c;
+  P->t = d_t;
+  P->n = n64;
+  P->cfg = *cfg;
+  P->k_lo = (long long)cfg->exclusion;
+  P->k_hi = L;
+  if (!(k_lo64 == 0 && k_hi64 == 0)) {
+    P->k_lo = std::max<long long>(P->k_lo, (long long)k_lo64);
+    P->k_hi = std::min<long long>(P->k_hi, (long long)k_hi64);
+  }
+  auto bail = [&](int32_t s2) { mprof_plan_destroy(P); return s2; };
+  if (cudaMalloc(&P->ws, workspace_bytes(L)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(fail(MPROF_E_OOM, "plan workspace of %zu bytes", workspace_bytes(L)));
+  }
+  Workspace w;
+  carve_at(static_cast<char*>(P->ws), L, &w);
+  uint32_t launches = 0;
+  st = prepare_operands(c, d_t, n, cfg, w, &launches);
+  c->stats_t = nullptr;  // the statistics live in the plan's workspace, not the context's
+  if (st != MPROF_OK) return bail(st);
+  const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  k_init_best<<<grid_for(L), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, L);
+  SeriesPlan sp;
+  st = plan_series(c, d_t, n, cfg, w, L, &launches, &sp);
+  if (st != MPROF_OK) return bail(st);
+  P->R = sp.R;
+  P->aamp_cov = c->aamp_cov;
+  P->zn_colscale = c->zn_colscale;
+  P->wide = c->wide;
+  P->probe_replays = c->probe_replays;
+  P->probe_cells = c->probe_cells;
+  if (P->k_lo < P->k_hi) {
+    const int k_tile = (!cfg->exact && P->k_lo == (long long)cfg->exclusion) ? (int)P->k_lo + 1 : (int)P->k_lo;
+    const Grid g = grid_of(c, cfg, L, L);
+    std::vector<int4> tl;
+    tile_list(g, k_tile, P->k_hi, P->R, tl, nullptr);
+    P->ntiles = (long long)tl.size();
+    const bool cov_main = zn ? !c->zn_colscale : c->aamp_cov;
+    if (cov_main && !cfg->exact && !knobs().zn_no_near)
+      while (P->n_near < P->ntiles && tl[P->n_near].x < g.g0 + kK) ++P->n_near;
+    if (!tl.empty()) {
+      if (cudaMalloc(&P->tiles, tl.size() * sizeof(int4)) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(MPROF_E_OOM, "plan tile table"));
+      }
+      const cudaError_t e = cudaMemcpyAsync(P->tiles, tl.data(), tl.size() * sizeof(int4),
+                                            cudaMemcpyHostToDevice, c->stream);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "plan tile table upload"));
+    }
+  }
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "mprof_plan_create"));
+  *out = P;
+  return MPROF_OK;
+}
+
+int32_t mprof_plan_sweep(mprof_plan* P, double* d_cmp, int64_t* d_idx, mprof_run_info* info) {
+  if (!P || !d_cmp || !d_idx) return fail(MPROF_E_BAD_ARG, "null argument");
+  mprof_ctx* c = P->ctx;
+  CK(cudaSetDevice(c->device));
+  const mprof_config* cfg = &P->cfg;
+  const int n = (int)P->n, L = n - (int)cfg->m + 1;
+  const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  c->aamp_cov = P->aamp_cov;  // with_policy / make_params read the form from the context
+  c->zn_colscale = P->zn_colscale;
+  c->wide = P->wide;
+  c->probe_replays = P->probe_replays;
+  c->probe_cells = P->probe_cells;
+  Workspace w;
+  carve_at(static_cast<char*>(P->ws), L, &w);
+  uint32_t launches = 0;
+  k_init_best<<<grid_for(L), 256, 0, c->stream>>>(w.best, zn ? w.B : nullptr, L);
+  ++launches;
+  SweepOut so;
+  so.R = P->R;
+  so.ntiles = P->ntiles;
+  if (P->k_lo < P->k_hi) {
+    SweepParams prm = make_params(c, P->t, n, cfg, w, (int)P->k_hi, L);
+    prm.tiles = P->tiles;
+    prm.R = (int)std::min<long long>(P->R, INT_MAX);
+    int32_t st = dispatch_sweep(c, cfg, prm, P->ntiles, P->n_near, (int)cfg->exclusion, true,
+                                &launches, &so.ms);
+    if (st != MPROF_OK) return st;
+    if (zn) {
+      st = flat_fix(c, w.B, L, (int)P->k_lo, (int)P->k_hi, w, w.best, &launches);
+      if (st != MPROF_OK) return st;
+    }
+  }
+  k_split<<<grid_for(L), 256, 0, c->stream>>>(w.best, d_cmp, d_idx, L);
+  ++launches;
+  CK(cudaGetLastError());
+  const uint64_t cells = P->k_lo < P->k_hi ? mprof_band_cells(P->n, cfg->m, (uint64_t)P->k_lo, (uint64_t)P->k_hi) : 0;
+  fill_info(c, cfg, cells, P->k_hi - P->k_lo, so, launches, info);
   return MPROF_OK;
 }
 

@@ -31,11 +31,12 @@
 
 namespace mpg {
 
-// Rows of a replayed block unrolled per iteration (replay_block; 1 = rolled, D = fully unrolled).
+// Rows of a replayed block unrolled per iteration (replay_block; 1 = rolled, 8 = fully unrolled;
+// 0 = by policy: unrolled for the covariance-only filters, whose replays the form probe keeps rare,
+// rolled otherwise -- see replay_block).
 #ifndef MPROF_REPLAY_UNROLL
-#define MPROF_REPLAY_UNROLL 1
+#define MPROF_REPLAY_UNROLL 0
 #endif
-constexpr int kReplayUnroll = MPROF_REPLAY_UNROLL;
 
 // ---------------------------------------------------------------------------------------------
 // Global profile entry: comparison-space value bits (non-negative double or +inf) and index.
@@ -176,10 +177,38 @@ __device__ __forceinline__ double abs_pow_exact(double x, double p) {
   else return pow(a, p);  // generic and half-integer p: std::pow, as the reference
 }
 
+// sqrt(a), a >= 0, for the half-integer p-norm path. MPROF_HALF_SQRT = 2 (default): the MUFU
+// double rsqrt seed (rsqrt.approx.f64) + two Newton steps in FP64, worst relative error 3.9e-16
+// over 1e-130..1e130 (tools/sqrt_check; C3 p = 2.5: 71 ms); 3: one Newton step (1.2e-12, 54 ms);
+// 1: a * rsqrt(a) (CUDA's double rsqrt, 123 ms); 0: IEEE sqrt (135 ms).
+#ifndef MPROF_HALF_SQRT
+#define MPROF_HALF_SQRT 2
+#endif
+__device__ __noinline__ double sqrt_rare(double a) { return sqrt(a); }
+__device__ __forceinline__ double sqrt_fast(double a) {
+  if constexpr (MPROF_HALF_SQRT == 1) {
+    return a > 0.0 ? a * rsqrt(a) : 0.0;
+  } else if constexpr (MPROF_HALF_SQRT == 2 || MPROF_HALF_SQRT == 3) {
+    // MUFU.RSQ64H seed (PTX rsqrt.approx.f64, full double range) + Newton steps in FP64
+    // zero and denormals (exponent field 0; the seed flushes them): the IEEE sqrt, out of line
+    // so that the hot path stays a not-taken branch (an inlined or predicated fallback measured
+    // 111 ms instead of 71 on C3 p = 2.5)
+    if (__double2hiint(a) < 0x00100000) return sqrt_rare(a);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    const double h = 0.5 * a;
+    y = y * fma(-h * y, y, 1.5);
+    if constexpr (MPROF_HALF_SQRT == 2) y = y * fma(-h * y, y, 1.5);
+    return a * y;
+  } else {
+    return sqrt(a);
+  }
+}
+
 // a^p (a >= 0) in the fast mode. PK = 1, 3, 4: exact products; PK = -k: the half-integer
-// p = k / 2 (k odd) as a^((k-1)/2) sqrt(a) (sqrt is correctly rounded: ~10 FP64-pipe
-// instructions instead of pow's ~100); PK = 0, any other p: exp2(p log2 a), relative error
-// ~ |p log2 a| 1e-16 against pow's ~1e-16 (the profile's tolerance is 1e-9).
+// p = k / 2 (k odd) as a^((k-1)/2) sqrt(a) (~10 FP64-pipe instructions instead of pow's ~100;
+// C3 p = 2.5: 746 -> 135 ms); PK = 0, any other p: pow (exp2(p log2 a) with CUDA's double
+// exp2 / log2 measured slower: C3 p = 2.7 746 -> 1286 ms).
 template <int PK>
 __device__ __forceinline__ double pow_fast(double a, double p) {
   if constexpr (PK == 1) return a;
@@ -187,13 +216,13 @@ __device__ __forceinline__ double pow_fast(double a, double p) {
   else if constexpr (PK == 4) { const double a2 = a * a; return a2 * a2; }
   else if constexpr (PK < 0) {
     constexpr int h = (-PK - 1) / 2;  // integer part of p
-    const double r = sqrt(a);
+    const double r = sqrt_fast(a);
     if constexpr (h == 0) return r;
     else if constexpr (h == 1) return a * r;
     else if constexpr (h == 2) return (a * a) * r;
     else return (a * a) * (a * r);
   } else {
-    return a == 0.0 ? 0.0 : exp2(p * log2(a));
+    return pow(a, p);
   }
 }
 
@@ -665,10 +694,14 @@ __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, in
   using V2 = typename P::V2;
   using VB = typename P::VB;
   if (stats) atomicAdd(&stats[0], 1ull);
-  // The row loop is rolled: a replay is the rare path, and its code must stay small -- on series
-  // where most blocks replay (noise-like data: loose thresholds everywhere) an unrolled 64-cell
-  // body thrashed the instruction cache (ncu: 61 % of stall samples "no instruction").
-#pragma unroll kReplayUnroll
+  // Unrolling the row loop pays where replays are rare and clustered (the covariance-only
+  // filters, confirmed by the form probe: C5 2101 vs 2317 ms, C4 ACAMP 118.8 vs 123.5 ms), but on
+  // series where most blocks replay (noise-like data, loose thresholds everywhere) the unrolled
+  // 64-cell body thrashes the instruction cache (ncu: 61 % of stall samples "no instruction";
+  // uniform noise n = 2^13, m = 256: 5.7 ms unrolled vs 2.15 ms rolled), so the other filters roll it.
+  constexpr bool kCovOnly = P::kCovFilter && !P::kColScale;
+  constexpr int kUnroll = MPROF_REPLAY_UNROLL ? MPROF_REPLAY_UNROLL : (kCovOnly ? D : 1);
+#pragma unroll kUnroll
   for (int u = 0; u < D; ++u) {
     if (GUARD && s + u >= cnt) break;
     const int x = s + u;

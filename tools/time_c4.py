@@ -25,5 +25,7 @@ for name in names:
         ms.append(res.info.sweep_ms)
     best = min(ms[1:])
     out[name] = {"sweep_ms": round(best, 3), "cells_per_s": f"{res.info.cells / (best * 1e-3):.4e}",
-                 "tiles": res.info.tiles, "R": res.info.rows_per_tile}
+                 "tiles": res.info.tiles, "R": res.info.rows_per_tile,
+                 "policy": getattr(res.info, "policy", "?"), "hg": getattr(res.info, "hit_group", 0),
+                 "probe": [getattr(res.info, "probe_replays", 0), getattr(res.info, "probe_cells", 0)]}
 print(json.dumps(out))
