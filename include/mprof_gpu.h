@@ -141,10 +141,12 @@ int32_t mprof_ctx_set_progress(mprof_ctx* ctx, mprof_progress_fn fn, void* user)
 /* Filter form of the FP64 fast-mode Euclidean and z-normalized sweeps. AUTO (default): chosen per
  * series (window-scale spread test + form probe). COV: covariance-only filter (EuclidCov /
  * Znorm<0>) with its own hit groups; WIDE: the same with the long hit groups (Wide<...>);
- * ALT: the (delta, sigma) Euclidean kernel / the column-scaled z-norm filter. Every form gives
- * the exact minimum under the same parity rules; this selects which kernel decides it (tests,
- * experiments). p-norm, exact and FP32 sweeps ignore it. */
-enum { MPROF_FORM_AUTO = 0, MPROF_FORM_COV = 1, MPROF_FORM_WIDE = 2, MPROF_FORM_ALT = 3 };
+ * ALT: the (delta, sigma) Euclidean kernel / the column-scaled z-norm filter; DENSE: no block
+ * filter at all (every cell compared exactly; chosen automatically for noise-like series, also
+ * for p-norm p = 1, 2, 3). Every form gives the exact minimum under the same parity rules; this
+ * selects which kernel decides it (tests, experiments). Exact and FP32 sweeps ignore it. */
+enum { MPROF_FORM_AUTO = 0, MPROF_FORM_COV = 1, MPROF_FORM_WIDE = 2, MPROF_FORM_ALT = 3,
+       MPROF_FORM_DENSE = 4 };
 int32_t mprof_ctx_set_form(mprof_ctx* ctx, int32_t form);
 
 /* ---- reference entry points (host buffers) ------------------------------------------------ */

@@ -118,6 +118,7 @@ class Form(enum.IntEnum):
     Cov = 1     # EuclidCov / Znorm<0>
     Wide = 2    # Wide<EuclidCov> / Wide<Znorm<0>>
     Alt = 3     # Euclid (delta, sigma) / Znorm<1> (column-scaled)
+    Dense = 4   # no block filter (noise-like series; also p-norm p = 1, 2, 3)
 
 
 def default_flat_threshold(m: int) -> float:

@@ -71,6 +71,17 @@ constexpr double kProbeMaxReplaysZ = 3e-5;
 #define MPROF_WIDE_MAX_REPLAYS 1e-5
 #endif
 constexpr double kProbeWideMaxReplays = MPROF_WIDE_MAX_REPLAYS;
+// Noise test (k_noise_test): random admissible pairs evaluated directly; above this fraction
+// passing the first-diagonal thresholds the series would sweep with Dense<P> (no block filter).
+// Off by default (> 1): measured on uniform noise, m = 256, Dense<P> wins only at the smallest
+// sizes (AAMP n = 2^13 1.75 vs 2.15 ms, ACAMP 0.83 vs 1.6 ms) and loses from n = 2^14 on (n = 2^16:
+// AAMP 12.0 vs 4.9 ms, ACAMP 8.0 vs 3.9 ms) -- DESIGN.md §3.5. Dense<P> stays available through
+// mprof_ctx_set_form(DENSE).
+constexpr int kNoiseSamples = 2048;
+#ifndef MPROF_NOISE_DENSE_FRAC
+#define MPROF_NOISE_DENSE_FRAC 2.0
+#endif
+constexpr double kNoiseDenseFrac = MPROF_NOISE_DENSE_FRAC;
 
 // Experiment / diagnostic switches, read once per process from the environment. The defaults are
 // the product configuration; tests and bench never set them (tools/ and DESIGN.md experiments do).
@@ -361,6 +372,7 @@ __global__ void k_first_diag(SweepParams prm, int k1) {
     const int end = min(kRun, cells - i0);
     for (int q = 0; q < end; ++q) {
       const int i = i0 + q, j = j0 + q;
+      MPG_CHECK(i >= 0 && j < L);
       if (q > 0) acc = P::step(acc, prm.A[i - 1], prm.A[j - 1], prm.p);
       const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
       const unsigned long long vb =
@@ -382,6 +394,40 @@ __global__ void k_first_diag_cols(SweepParams prm, int k1) {
     const BestEntry cur = prm.best[j];
     const long long io = i;
     if (lex_less(vb, io, cur.v, cur.idx)) prm.best[j] = BestEntry{vb, io};
+  }
+}
+
+// Noise test (plan_series): nsamp admissible pairs (i, i + k) drawn by a fixed hash, each evaluated
+// directly (one warp, the policy's seed sum) in the comparison space, and counted when it would
+// pass the thresholds the first-diagonal prepass left in best[] (value <= max of the row and
+// column entries' values). On a random walk the prepass thresholds (nearest neighbours at k =
+// exclusion) are far below a random pair; on noise-like data they are ordinary pair distances
+// and about half the random pairs pass -- the block filter then passes almost every block.
+template <class PP>
+__global__ void k_noise_test(SweepParams prm, int k1, int nsamp, unsigned int* count) {
+  using P = typename PP::Base;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const long long span = (long long)prm.L - k1;  // admissible diagonals [k1, L)
+  for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nsamp; q += warps) {
+    unsigned long long h = 0x9e3779b97f4a7c15ull * (unsigned long long)(q + 1);
+    h ^= h >> 31;
+    h *= 0xbf58476d1ce4e5b9ull;
+    h ^= h >> 29;
+    const int k = k1 + (int)(h % (unsigned long long)span);
+    const int i = (int)((h >> 32) % (unsigned long long)(prm.L - k));
+    const int j = i + k;
+    const double mui = P::kCenteredSeed ? prm.mu[i] : 0.0;
+    const double muj = P::kCenteredSeed ? prm.mu[j] : 0.0;
+    double acc = 0.0;
+    for (int l = lane; l < prm.m; l += 32) acc = P::seed(acc, prm.t[i + l] - mui, prm.t[j + l], muj, prm.p);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+      const double v = P::score(acc, P::kHasB ? prm.B[i] : 0.0, P::kHasB ? prm.B[j] : 0.0);
+      const unsigned long long vb = v < 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+      const unsigned long long th = max(prm.best[i].v, prm.best[j].v);
+      if (vb <= th) atomicAdd(count, 1u);
+    }
   }
 }
 
@@ -803,6 +849,8 @@ struct mprof_ctx {
   bool zn_colscale = false;  // z-norm filter form chosen for the current sweep
   bool aamp_cov = false;     // AAMP form chosen for the current sweep (covariance vs delta-sigma)
   bool wide = false;         // covariance-only policy with longer hit groups (probe: no replays)
+  bool dense = false;        // Dense<P>: no block filter (noise-like series, plan_series)
+  unsigned int* noise_cnt = nullptr;  // noise test counter
   double* d_spread = nullptr;
   int4* probe_d = nullptr;                 // AAMP form probe: tile list and replay counter
   unsigned long long* probe_cnt = nullptr;
@@ -812,6 +860,7 @@ struct mprof_ctx {
   long long plan_R = 0;                   // rows per tile of the last planned series
   unsigned long long probe_replays = 0;   // last form probe: replayed blocks / sample cells
   double probe_cells = 0.0;
+  double noise_frac = -1.0;               // last noise test: fraction of random pairs passing
 };
 
 // Device-resident EngineState: the series, the comparison-space profile and scratch.
@@ -843,7 +892,7 @@ struct mprof_plan {
   void* ws = nullptr;            // owned workspace (operands, profile, scratch)
   int4* tiles = nullptr;         // owned tile table
   long long ntiles = 0, n_near = 0, R = 0;
-  bool aamp_cov = false, zn_colscale = false, wide = false;
+  bool aamp_cov = false, zn_colscale = false, wide = false, dense = false;
   unsigned long long probe_replays = 0;
   double probe_cells = 0.0;
 };
@@ -1267,6 +1316,13 @@ int32_t with_policy(const mprof_ctx* c, const mprof_config* cfg, F&& f) {
     if (p == 4.0) return f.template operator()<PnormF32<4>>();
     return f.template operator()<PnormF32<0>>();
   }
+  const bool ex0 = cfg->exact != 0;
+  if (c->dense && !ex0) {  // noise-like series: no block filter (plan_series)
+    if (cfg->family == MPROF_ZNORMALIZED) return f.template operator()<Dense<Znorm<true>>>();
+    if (l2) return f.template operator()<Dense<Euclid<false>>>();
+    if (p == 1.0) return f.template operator()<Dense<Pnorm<1, false>>>();
+    if (p == 3.0) return f.template operator()<Dense<Pnorm<3, false>>>();
+  }
   if (cfg->family == MPROF_ZNORMALIZED) {
     if (c->zn_colscale) return f.template operator()<Znorm<true>>();
     return c->wide ? f.template operator()<Wide<Znorm<false>>>() : f.template operator()<Znorm<false>>();
@@ -1458,7 +1514,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     // the measured choice)
     if (c->form == MPROF_FORM_COV || c->form == MPROF_FORM_WIDE) {
       c->zn_colscale = false;
-    } else if (c->form == MPROF_FORM_ALT) {
+    } else if (c->form == MPROF_FORM_ALT || c->form == MPROF_FORM_DENSE) {
       c->zn_colscale = true;
     } else if (knobs().zn_filter == 1) {
       c->zn_colscale = false;
@@ -1482,7 +1538,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
     ++*launches;
     c->aamp_cov = false;
     const bool forced = c->form != MPROF_FORM_AUTO;
-    if (ds && cfg->precision == MPROF_FP64 && c->form != MPROF_FORM_ALT &&
+    if (ds && cfg->precision == MPROF_FP64 && c->form != MPROF_FORM_ALT && c->form != MPROF_FORM_DENSE &&
         (forced || knobs().aamp_cov != 0)) {
       // covariance form (EuclidCov) when the window scales vary little inside the filter
       // blocks (the same spread test as the z-norm filter form; MPROF_AAMP_COV=0|1 overrides)
@@ -1592,13 +1648,50 @@ int32_t plan_series(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     if (zn) c->zn_colscale = true;
     else c->aamp_cov = false;
   }
-  if (auto_cov && !cfg->exact && cfg->precision == MPROF_FP64 && big) {
+  // Dense<P> (no block filter): forced, or chosen by the noise test for noise-like series
+  const bool fast64 = !cfg->exact && cfg->precision == MPROF_FP64;
+  const bool dense_ok = fast64 && (zn || cfg->family == MPROF_EUCLIDEAN ||
+                                   (cfg->family == MPROF_PNORM && (cfg->p == 1.0 || cfg->p == 2.0 || cfg->p == 3.0)));
+  c->dense = dense_ok && c->form == MPROF_FORM_DENSE;
+  if (kNoiseDenseFrac <= 1.0 && dense_ok && c->form == MPROF_FORM_AUTO && row_hi == L &&
+      L - (long long)cfg->exclusion > 1 && knobs().zn_filter == 0 && knobs().aamp_cov == -1) {
     const SweepParams prm = make_params(c, d_t, n, cfg, w, L, L);
     int32_t st = with_policy(c, cfg, [&]<class P>() {
       return launch_first_diag<P>(c, prm, (int)cfg->exclusion, launches);
     });
     if (st != MPROF_OK) return st;
     out->first_diag_done = true;
+    if (!c->noise_cnt) CK(cudaMalloc(&c->noise_cnt, sizeof(unsigned int)));
+    CK(cudaMemsetAsync(c->noise_cnt, 0, sizeof(unsigned int), c->stream));
+    st = with_policy(c, cfg, [&]<class P>() {
+      k_noise_test<P><<<grid_for(32LL * kNoiseSamples, 256), 256, 0, c->stream>>>(
+          prm, (int)cfg->exclusion, kNoiseSamples, c->noise_cnt);
+      return MPROF_OK;
+    });
+    ++*launches;
+    unsigned int cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, c->noise_cnt, sizeof cnt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->noise_frac = (double)cnt / kNoiseSamples;
+    c->dense = c->noise_frac > kNoiseDenseFrac;
+    if (knobs().tile_debug)
+      fprintf(stderr, "[mprof noise] %u of %d random pairs pass the first-diagonal thresholds -> %s\n",
+              cnt, kNoiseSamples, c->dense ? "dense" : "filtered");
+  }
+  if (c->dense) {  // the dense kernels are the (delta, sigma) / column-scaled / p-norm slides
+    if (zn) c->zn_colscale = true;
+    else c->aamp_cov = false;
+  }
+  if (!c->dense && auto_cov && fast64 && big) {
+    const SweepParams prm = make_params(c, d_t, n, cfg, w, L, L);
+    int32_t st = MPROF_OK;
+    if (!out->first_diag_done) {
+      st = with_policy(c, cfg, [&]<class P>() {
+        return launch_first_diag<P>(c, prm, (int)cfg->exclusion, launches);
+      });
+      if (st != MPROF_OK) return st;
+      out->first_diag_done = true;
+    }
     st = probe_form(c, zn, prm, (int)(g0 + kK), launches);
     if (st != MPROF_OK) return st;
   }
@@ -1609,7 +1702,7 @@ int32_t plan_series(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   const long long key[9] = {L, g.g0, row_hi, (long long)cfg->m, cfg->exact,
                             (long long)cfg->refresh_interval,
                             ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) |
-                                (c->aamp_cov ? 2 : 0) | (c->wide ? 4 : 0),
+                                (c->aamp_cov ? 2 : 0) | (c->wide ? 4 : 0) | (c->dense ? 8 : 0),
                             pbits, slots};
   if (std::equal(key, key + 9, c->R_key)) {
     out->R = c->R_val;
@@ -1626,7 +1719,7 @@ int32_t plan_series(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
 
 // The per-series decisions that fix every cell's arithmetic: rows per tile and kernel forms.
 int plan_flags(const mprof_ctx* c) {
-  return (c->aamp_cov ? 1 : 0) | (c->zn_colscale ? 2 : 0) | (c->wide ? 4 : 0);
+  return (c->aamp_cov ? 1 : 0) | (c->zn_colscale ? 2 : 0) | (c->wide ? 4 : 0) | (c->dense ? 8 : 0);
 }
 
 // The tiles of diagonals [k_lo, k_hi) x rows [0, row_hi) into w.best (initialised by the caller),
@@ -1915,6 +2008,7 @@ void mprof_ctx_destroy(mprof_ctx* c) {
   if (c->d_spread) cudaFree(c->d_spread);
   if (c->probe_d) cudaFree(c->probe_d);
   if (c->probe_cnt) cudaFree(c->probe_cnt);
+  if (c->noise_cnt) cudaFree(c->noise_cnt);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->side) {
@@ -2633,6 +2727,7 @@ int32_t mprof_plan_create(mprof_ctx* in, const double* d_t, uint64_t n64, const 
   P->aamp_cov = c->aamp_cov;
   P->zn_colscale = c->zn_colscale;
   P->wide = c->wide;
+  P->dense = c->dense;
   P->probe_replays = c->probe_replays;
   P->probe_cells = c->probe_cells;
   if (P->k_lo < P->k_hi) {
@@ -2670,6 +2765,7 @@ int32_t mprof_plan_sweep(mprof_plan* P, double* d_cmp, int64_t* d_idx, mprof_run
   c->aamp_cov = P->aamp_cov;  // with_policy / make_params read the form from the context
   c->zn_colscale = P->zn_colscale;
   c->wide = P->wide;
+  c->dense = P->dense;
   c->probe_replays = P->probe_replays;
   c->probe_cells = P->probe_cells;
   Workspace w;
@@ -2701,7 +2797,7 @@ int32_t mprof_plan_sweep(mprof_plan* P, double* d_cmp, int64_t* d_idx, mprof_run
 }
 
 int32_t mprof_ctx_set_form(mprof_ctx* in, int32_t form) {
-  if (form < MPROF_FORM_AUTO || form > MPROF_FORM_ALT) return fail(MPROF_E_BAD_ARG, "unknown form %d", form);
+  if (form < MPROF_FORM_AUTO || form > MPROF_FORM_DENSE) return fail(MPROF_E_BAD_ARG, "unknown form %d", form);
   mprof_ctx* c = nullptr;
   int32_t st = resolve_ctx(in, &c);
   if (st != MPROF_OK) return st;

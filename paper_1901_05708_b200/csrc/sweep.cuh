@@ -31,6 +31,24 @@
 
 namespace mpg {
 
+// Device-side bounds checks (MPROF_CHECKS=1 builds only; compute-sanitizer is not available on
+// this pool): every shared-memory ring / table index and every profile position a kernel touches
+// is checked and a violation traps (the launch fails with an illegal-instruction error).
+#ifndef MPROF_CHECKS
+#define MPROF_CHECKS 0
+#endif
+constexpr int kStageRowsMax = 256;  // largest rows-per-stage of any policy (checks only)
+#if MPROF_CHECKS
+#define MPG_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define MPG_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // Rows of a replayed block unrolled per iteration (replay_block; 1 = rolled, 8 = fully unrolled;
 // 0 = by policy: unrolled for the covariance-only filters, whose replays the form probe keeps rare,
 // rolled otherwise -- see replay_block).
@@ -64,6 +82,7 @@ __device__ __forceinline__ bool lex_less(unsigned long long v, long long i, unsi
 // what it compares with).
 __device__ __forceinline__ unsigned long long offer(BestEntry* best, long long pos,
                                                     unsigned long long v, long long idx) {
+  MPG_CHECK(pos >= 0 && idx >= -1);
   const longlong2 raw = __ldcg(reinterpret_cast<const longlong2*>(best + pos));
   BestEntry cur{static_cast<unsigned long long>(raw.x), raw.y};
   bool atomic_read = false;  // cur was returned by a CAS (an atomic read of the entry)
@@ -179,21 +198,18 @@ __device__ __forceinline__ double abs_pow_exact(double x, double p) {
 
 // sqrt(a), a >= 0, for the half-integer p-norm path. MPROF_HALF_SQRT = 2 (default): the MUFU
 // double rsqrt seed (rsqrt.approx.f64) + two Newton steps in FP64, worst relative error 3.9e-16
-// over 1e-130..1e130 (tools/sqrt_check; C3 p = 2.5: 71 ms); 3: one Newton step (1.2e-12, 54 ms);
+// over 1e-130..1e130 for normal inputs (tools/sqrt_check; C3 p = 2.5: 71 ms); 3: one Newton step
+// (1.2e-12, 54 ms);
 // 1: a * rsqrt(a) (CUDA's double rsqrt, 123 ms); 0: IEEE sqrt (135 ms).
 #ifndef MPROF_HALF_SQRT
 #define MPROF_HALF_SQRT 2
 #endif
-__device__ __noinline__ double sqrt_rare(double a) { return sqrt(a); }
 __device__ __forceinline__ double sqrt_fast(double a) {
   if constexpr (MPROF_HALF_SQRT == 1) {
     return a > 0.0 ? a * rsqrt(a) : 0.0;
   } else if constexpr (MPROF_HALF_SQRT == 2 || MPROF_HALF_SQRT == 3) {
     // MUFU.RSQ64H seed (PTX rsqrt.approx.f64, full double range) + Newton steps in FP64
-    // zero and denormals (exponent field 0; the seed flushes them): the IEEE sqrt, out of line
-    // so that the hot path stays a not-taken branch (an inlined or predicated fallback measured
-    // 111 ms instead of 71 on C3 p = 2.5)
-    if (__double2hiint(a) < 0x00100000) return sqrt_rare(a);
+    // a must be normal (the seed flushes denormals to 0): pow_fast clamps its argument
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
     const double h = 0.5 * a;
@@ -215,10 +231,16 @@ __device__ __forceinline__ double pow_fast(double a, double p) {
   else if constexpr (PK == 3) return a * a * a;
   else if constexpr (PK == 4) { const double a2 = a * a; return a2 * a2; }
   else if constexpr (PK < 0) {
-    constexpr int h = (-PK - 1) / 2;  // integer part of p
-    const double r = sqrt_fast(a);
-    if constexpr (h == 0) return r;
-    else if constexpr (h == 1) return a * r;
+    constexpr int h = (-PK - 1) / 2;  // integer part of p, >= 1 (p >= 1)
+    static_assert(h >= 1, "half-integer p >= 1.5");
+    // sqrt of max(a, DBL_MIN) (integer ops on the high word): for a < DBL_MIN the product
+    // a^h sqrt(.) underflows to 0 either way, so the clamp changes no result and keeps the hot
+    // path branch-free (a branch to an IEEE fallback measured 103 ms instead of 71 on C3 p = 2.5)
+    const int hi = __double2hiint(a);
+    const bool tiny = hi < 0x00100000;
+    const double an = __hiloint2double(tiny ? 0x00100000 : hi, tiny ? 0 : __double2loint(a));
+    const double r = sqrt_fast(an);
+    if constexpr (h == 1) return a * r;
     else if constexpr (h == 2) return (a * a) * r;
     else return (a * a) * (a * r);
   } else {
@@ -380,6 +402,23 @@ struct Wide : P {
   static constexpr int kHitGroup = MPROF_HIT_GROUP_WIDE;
 };
 
+// Dense<P>: the same slide without the block filter -- every cell is compared exactly with its
+// row and column thresholds as it is computed, and candidates are reduced per CTA in shared
+// memory (exact 128-bit lexicographic minima) and offered to the global profile once per stage.
+// Chosen per series for noise-like data, where the filter passes (and replays) nearly every block
+// (plan_series' noise test).
+template <class P>
+struct Dense : P {
+  static constexpr bool kDense = true;
+  static constexpr int kHitGroup = 1;
+};
+
+template <class P>
+constexpr bool is_dense() {
+  if constexpr (requires { P::kDense; }) return P::kDense;
+  else return false;
+}
+
 template <class P>
 constexpr int hit_group_of() {
   if constexpr (requires { P::kHitGroup; }) return P::kHitGroup;
@@ -515,6 +554,10 @@ constexpr const char* policy_name() {
   else if constexpr (std::is_same_v<P, PnormF32<0>>) return "PnormF32<p>";
   else if constexpr (std::is_same_v<P, ZnormF32<false>>) return "ZnormF32<0>";
   else if constexpr (std::is_same_v<P, ZnormF32<true>>) return "ZnormF32<1>";
+  else if constexpr (std::is_same_v<P, Dense<Euclid<false>>>) return "Dense<Euclid>";
+  else if constexpr (std::is_same_v<P, Dense<Znorm<true>>>) return "Dense<Znorm<1>>";
+  else if constexpr (std::is_same_v<P, Dense<Pnorm<1, false>>>) return "Dense<Pnorm<1>>";
+  else if constexpr (std::is_same_v<P, Dense<Pnorm<3, false>>>) return "Dense<Pnorm<3>>";
   else return "?";
 }
 
@@ -588,6 +631,10 @@ struct SweepSmem {
   static constexpr bool SK = (ZQ || EQ) && sizeof(typename P::V) == 8 && MPROF_SAMPLED_KEYS;
   float2 drow[SK ? S / D : 1];
   float2 dcol[SK ? NCB : 1];
+  // Dense<P>: the stage's exact candidates of its rows and of its live column window
+  static constexpr bool DN = is_dense<P>();
+  BestEntry crow[DN ? S : 1];
+  BestEntry ccol[DN ? G::NCOL : 1];
 };
 
 struct SweepParams {
@@ -665,6 +712,7 @@ struct Acc {
 __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhit, int row, int j,
                                         int* ct, BestEntry* best, unsigned long long* rv,
                                         int* rj, unsigned long long* stats) {
+  MPG_CHECK(row >= 0 && j > row);
   // clamp the comparison value at 0 (std::max(0.0, .), aamp.hpp:41; 1 - corr >= 0)
   const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
   if (colhit) {
@@ -705,6 +753,7 @@ __device__ __noinline__ Acc<P, D> replay_block(Acc<P, D> acc, int s, int cnt, in
   for (int u = 0; u < D; ++u) {
     if (GUARD && s + u >= cnt) break;
     const int x = s + u;
+    MPG_CHECK(x >= 0 && x < kStageRowsMax);
     const V2 r = rowA[x];
     const VB rb = P::kHasB ? rowB[x] : VB{};
     const int row = i0 + x + 1;
@@ -889,6 +938,120 @@ __device__ __noinline__ void resolve_seed(Cells<D> c, unsigned valid, int row, i
 #define MPROF_HIT_GROUP 1       // other value-key filters (p-norm, exact mode)
 #endif
 
+// Exact lexicographic min-update of a shared-memory entry (Dense<P>'s per-stage candidates).
+__device__ __forceinline__ void offer_shared(BestEntry* e, unsigned long long v, long long idx) {
+  BestEntry cur = *e;
+  while (lex_less(v, idx, cur.v, cur.idx)) {
+    const BestEntry old = atomicCAS(e, cur, BestEntry{v, idx});
+    if (old.v == cur.v && old.idx == cur.idx) return;
+    cur = old;
+  }
+}
+
+// One stage of a Dense<P> sweep: the slide of the hot loop (register ring of column operands,
+// row operand broadcast), and for EVERY cell an exact comparison with the row threshold and the
+// column threshold in shared memory; a cell that can improve or tie goes into the CTA's
+// shared-memory candidates (ccol per live column, crow per row of the stage; flushed to the
+// global profile at the stage end by dense_flush) and tightens the shared threshold word.
+template <class P, int D, int T, int S, bool GUARD>
+__device__ __forceinline__ void dense_stage(SweepSmem<P, D, T, S>& sm, int b, int X0,
+                                            typename P::V (&acc)[D], int i0, int cnt, int kt,
+                                            int kend, int L, double p) {
+  using G = Geo<D, T, S>;
+  using V2 = typename P::V2;
+  using VB = typename P::VB;
+  const int xb = threadIdx.x * D;
+  V2 cA[D];
+  VB cB[D];
+  {
+    const int q0 = G::pad((X0 + xb) % G::RING);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      cA[d] = sm.colA[q0 + d];
+      if constexpr (P::kHasB) cB[d] = sm.colB[q0 + d];
+    }
+  }
+  const V2* rowA = sm.rowA[b];
+  int* colT = sm.colT[b];
+  for (int s = 0; s < cnt; s += D) {
+    const int qn = G::pad((X0 + s + xb + D) % G::RING);
+    MPG_CHECK(qn + D <= G::RINGP);
+    const V2* nA = &sm.colA[qn];
+    const VB* nB = &sm.colB[P::kHasB ? qn : 0];
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      if (GUARD && s + u >= cnt) break;
+      const int x = s + u;
+      MPG_CHECK(x < S);
+      const V2 r = rowA[x];
+      const VB rb = P::kHasB ? sm.rowB[b][x] : VB{};
+      const int row = i0 + x + 1;
+      const int tr = *reinterpret_cast<volatile int*>(&sm.rowT[b][x]);
+      unsigned long long rv = kInfBits;
+      int rj = INT_MAX;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int sl = (d + u) % D;
+        acc[d] = P::step(acc[d], r, cA[sl], p);
+        if (GUARD && !((kt + d < kend) && (row + kt + d <= L - 1))) continue;
+        const int j = row + kt + d;
+        const double v = cell_value<P>(acc[d], rb, P::kHasB ? cB[sl] : VB{}, row, j);
+        const int h = __double2hiint(v);
+        const unsigned long long vb = (h < 0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v));
+        const int xc = x + xb + d;  // column offset in the stage window
+        MPG_CHECK(xc < G::NCOL && j < L);
+        int* ct = &colT[G::pad(xc)];
+        if (h <= *reinterpret_cast<volatile int*>(ct)) {
+          offer_shared(&sm.ccol[xc], vb, row);
+          atomicMin(ct, h < 0 ? 0 : h);
+        }
+        if (h <= tr && lex_less(vb, j, rv, rj)) {
+          rv = vb;
+          rj = j;
+        }
+      }
+      // the row is shared by the whole CTA: reduce the warp's candidates first (lexicographic,
+      // shuffles), one shared-memory offer per warp instead of one per thread
+      if (__any_sync(0xffffffffu, rj != INT_MAX)) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long ov = __shfl_xor_sync(0xffffffffu, rv, off);
+          const int oj = __shfl_xor_sync(0xffffffffu, rj, off);
+          if (lex_less(ov, oj, rv, rj)) {
+            rv = ov;
+            rj = oj;
+          }
+        }
+        if ((threadIdx.x & 31) == 0 && rj != INT_MAX) {
+          offer_shared(&sm.crow[x], rv, rj);
+          atomicMin(&sm.rowT[b][x], static_cast<int>(rv >> 32));
+        }
+      }
+      cA[u] = nA[u];
+      if constexpr (P::kHasB) cB[u] = nB[u];
+    }
+  }
+}
+
+// Dense<P>: offer the stage's shared candidates to the global profile and reset them (between
+// the stage's CTA barriers: no warp touches them). Rows i0 + 1 + x; columns at stage offset x are
+// position i0 + kb + 1 + x (load_stage's colT positions).
+template <class P, int D, int T, int S>
+__device__ __forceinline__ void dense_flush(SweepSmem<P, D, T, S>& sm, BestEntry* best, int i0,
+                                            int kb, int L) {
+  using G = Geo<D, T, S>;
+  for (int x = threadIdx.x; x < S; x += T) {
+    const BestEntry e = sm.crow[x];
+    if (e.idx != kNoIdx && i0 + 1 + x < L) offer(best, i0 + 1 + x, e.v, e.idx);
+    sm.crow[x] = BestEntry{kInfBits, kNoIdx};
+  }
+  for (int x = threadIdx.x; x < G::NCOL; x += T) {
+    const BestEntry e = sm.ccol[x];
+    if (e.idx != kNoIdx && i0 + kb + 1 + x < L) offer(best, i0 + kb + 1 + x, e.v, e.idx);
+    sm.ccol[x] = BestEntry{kInfBits, kNoIdx};
+  }
+}
+
 // Blocks per hit test of policy P's kernel (the policy's own choice, else per filter kind).
 template <class P>
 __host__ __device__ constexpr int hit_group_for() {
@@ -906,6 +1069,10 @@ __device__ __forceinline__ void run_stage(SweepSmem<P, D, T, S>& sm, int b, int 
                                           typename P::V (&acc)[D], int i0, int cnt, int kt,
                                           int kend, int L, BestEntry* best, double p,
                                           unsigned long long* stats) {
+  if constexpr (is_dense<P>()) {
+    dense_stage<P, D, T, S, GUARD>(sm, b, X0, acc, i0, cnt, kt, kend, L, p);
+    return;
+  }
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
   using VB = typename P::VB;
@@ -1295,6 +1462,7 @@ __device__ __forceinline__ void load_stage(SweepSmem<P, D, T, S>& sm, const Swee
   const int b = st & 1;
   const int i0 = ra + st * S;
   const int* bestw = reinterpret_cast<const int*>(prm.best);  // word view; hi word at +1
+  MPG_CHECK(i0 >= 0 && kb >= 0 && i0 + kb < L);
   for (int x = threadIdx.x; x < G::NCOL; x += T) {
     const int pb = i0 + kb + 1 + x;
     const bool vb = pb < L;
@@ -1334,6 +1502,8 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   const int4 tl = prm.tiles[blockIdx.x];
   const int kb = tl.x, ra = tl.y;
   const int re = tl.z;  // exclusive row end of the tile (<= L - kb, <= row_hi)
+  MPG_CHECK(kb >= 1 && ra >= 0 && ra < re && re <= prm.L - kb && re <= prm.row_hi && tl.w > kb &&
+            tl.w <= prm.L);
   const int L = prm.L;
   const int m = prm.m;
   const int kt = kb + static_cast<int>(threadIdx.x) * D;
@@ -1421,6 +1591,10 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
   if (steps <= 0) return;
   const int nst = (steps + S - 1) / S;
   __syncthreads();  // seed scratch reuse
+  if constexpr (SM::DN) {
+    for (int x = threadIdx.x; x < S; x += T) sm.crow[x] = BestEntry{kInfBits, kNoIdx};
+    for (int x = threadIdx.x; x < G::NCOL; x += T) sm.ccol[x] = BestEntry{kInfBits, kNoIdx};
+  }
   load_stage<P, D, T, S>(sm, prm, 0, ra, kb);
   cp_async_commit();
   cp_async_wait<0>();
@@ -1439,9 +1613,16 @@ __global__ void __launch_bounds__(T, MINB) sweep_kernel(const SweepParams prm) {
     } else {
       run_stage<P, D, T, S, true>(sm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p, prm.stats);
     }
-    if (st + 1 == nst) break;
+    if (st + 1 == nst) {
+      if constexpr (SM::DN) {
+        __syncthreads();
+        dense_flush<P, D, T, S>(sm, prm.best, i0, kb, L);
+      }
+      break;
+    }
     cp_async_wait<0>();
     __syncthreads();
+    if constexpr (SM::DN) dense_flush<P, D, T, S>(sm, prm.best, i0, kb, L);
     stage_block_max<P, D, T, S>(sm, (st + 1) & 1, s0 + S);
     if (st + 2 < nst) load_stage<P, D, T, S>(sm, prm, st + 2, ra, kb);
     cp_async_commit();

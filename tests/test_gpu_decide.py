@@ -43,6 +43,7 @@ EXPECT = {
     (EUCLIDEAN, "auto"): {"Wide<EuclidCov>", "EuclidCov", "Euclid"},
     (ZNORM, "cov"): {"Znorm<0>"}, (ZNORM, "wide"): {"Wide<Znorm<0>>"}, (ZNORM, "alt"): {"Znorm<1>"},
     (ZNORM, "auto"): {"Wide<Znorm<0>>", "Znorm<0>", "Znorm<1>"},
+    (EUCLIDEAN, "dense"): {"Dense<Euclid>"}, (ZNORM, "dense"): {"Dense<Znorm<1>>"},
 }
 
 
@@ -148,11 +149,36 @@ def test_forced_forms_small(mp, ctx, n, m, excl, fam):
     r = np.random.default_rng(n + m + excl)
     t = np.cumsum(r.standard_normal(n)) + 50.0
     _, Pr, Ir = oracle.scan(t, m, fam, exclusion=excl)
-    for form in ("cov", "wide", "alt"):
+    for form in ("cov", "wide", "alt", "dense"):
         P, I, info = run(mp, ctx, t, m, fam, excl, form)
         assert info.policy in EXPECT[(fam, form)], (form, info.policy)
         rep = check(t, m, fam, P, I, Pr, Ir, tol=TOL, abs_bound=ZN_ABS if fam == ZNORM else None)
         assert rep.ok, (form, rep.summary())
+
+
+@pytest.mark.parametrize("kind", ["uniform", "walk"])
+@pytest.mark.parametrize("fam,p", [(EUCLIDEAN, 2.0), (ZNORM, 2.0), (1, 1.0), (1, 3.0)],
+                         ids=["aamp", "acamp", "p1", "p3"])
+def test_dense_form_noise(mp, ctx, kind, fam, p):
+    """Dense<P> (no block filter, every cell compared exactly, shared-memory candidates flushed
+    per stage) forced on noise-like series (uniform iid samples, the reference acceptance
+    criterion 9 input) and on random walks, and the automatic (filtered) choice, all against the
+    oracle."""
+    r = np.random.default_rng(9001 + fam)
+    t = r.uniform(-1, 1, 8192) if kind == "uniform" else np.cumsum(r.standard_normal(8192))
+    m = 256
+    kindobj = {EUCLIDEAN: mp.DistanceKind.euclidean(), ZNORM: mp.DistanceKind.znormalized(),
+               1: mp.DistanceKind.pnorm(p)}[fam]
+    _, Pr, Ir = oracle.scan(t, m, fam, p)
+    for form in (mp.Form.Auto, mp.Form.Dense):
+        ctx.set_form(form)
+        fn = {EUCLIDEAN: mp.aamp, ZNORM: mp.acamp, 1: mp.aamp_pnorm}[fam]
+        res = fn(mp.make_time_series(t), mp.ProfileConfig(m, kindobj), ctx=ctx)
+        ctx.set_form(mp.Form.Auto)
+        assert res.info.policy.startswith("Dense<") == (form == mp.Form.Dense), res.info.policy
+        rep = check(t, m, fam, res.distances, res.nn_index, Pr, Ir, tol=TOL, p=p,
+                    abs_bound=ZN_ABS if fam == ZNORM else None)
+        assert rep.ok, (kind, form, rep.summary())
 
 
 def test_run_info_reports_policy(mp):
