@@ -49,8 +49,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--engines", default="aamp,acamp")
-    ap.add_argument("--n", type=int, default=N_C4)
-    ap.add_argument("--m", type=int, default=M_C4)
+    # (--series-len / --window: the spellings to use under torchrun, whose own parser rejects
+    # "--n" / "--m" as ambiguous abbreviations of its options)
+    ap.add_argument("--n", "--series-len", dest="n", type=int, default=N_C4)
+    ap.add_argument("--m", "--window", dest="m", type=int, default=M_C4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-configs", action="store_true",

@@ -509,6 +509,7 @@ class Plan:
                  ctx: Optional[Context] = None):
         self.cfg = cfg
         self._c = _to_c(cfg)
+        self._ctx = ctx  # the plan borrows the context: keep it alive as long as the plan
         h = C.c_void_p()
         _raise(lib().mprof_plan_create(_ctx_handle(ctx), C.c_void_p(d_t), n, C.byref(self._c),
                                        k_lo, k_hi, C.byref(h)))

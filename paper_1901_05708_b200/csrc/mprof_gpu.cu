@@ -6,6 +6,8 @@
 //   -> sweep_kernel (all tiles) -> [z-norm flat-pair rule] -> split to (cmp, idx)
 //   -> finalize (comparison value -> distance).
 #include <cuda_runtime.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <climits>
@@ -835,13 +837,25 @@ struct mprof_ctx {
   // host-API staging
   void* io = nullptr;
   size_t io_bytes = 0;
-  // tile table cache
-  std::vector<int4> tiles_h;  // (first diagonal, first row, row end, -)
-  int4* tiles_d = nullptr;
-  size_t tiles_cap = 0;
-  long long tiles_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
-  long long R_key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // rows-per-tile choice cache
-  long long R_val = 0;
+  // Tile table cache: a few tables (least recently used replaced), so callers alternating
+  // between engines or series shapes on one context (AAMP then ACAMP of the same series, the
+  // usual host-API pattern) neither rebuild and re-upload the table nor rerun the schedule model.
+  struct TileSlot {
+    std::vector<int4> h;  // (first diagonal, first row, row end, diagonal end)
+    int4* d = nullptr;
+    size_t cap = 0;
+    long long key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+    unsigned long long used = 0;
+  };
+  static constexpr int kTileSlots = 4;
+  TileSlot tile_slot[kTileSlots];
+  TileSlot* tiles = &tile_slot[0];  // the table of the current sweep
+  unsigned long long tile_clock = 0;
+  struct RChoice {  // rows-per-tile choice cache
+    long long key[9];
+    long long R;
+  };
+  std::vector<RChoice> R_cache;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
   const double* stats_t = nullptr;
   uint64_t stats_n = 0, stats_m = 0;
@@ -884,7 +898,8 @@ struct mprof_state {
 // A planned band sweep of one series (mprof_plan_create): the per-series decisions, the prepared
 // operands and the band's tile table, so that mprof_plan_sweep only enqueues kernels.
 struct mprof_plan {
-  mprof_ctx* ctx = nullptr;  // borrowed
+  mprof_ctx* ctx = nullptr;  // borrowed: must outlive every mprof_plan_sweep (not the destroy)
+  int device = 0;
   const double* t = nullptr;
   uint64_t n = 0;
   mprof_config cfg;
@@ -939,6 +954,12 @@ int32_t resolve_ctx(mprof_ctx* in, mprof_ctx** out) {
 }
 
 DefaultContexts::~DefaultContexts() {
+  // The main thread's thread-locals are destroyed while the process exits, when the CUDA runtime
+  // (or the embedding interpreter's) may already be tearing down: leave those to the driver.
+  if (static_cast<long>(syscall(SYS_gettid)) == static_cast<long>(getpid())) {
+    by_device.clear();
+    return;
+  }
   // mprof_ctx_destroy erases its entry: take the contexts out first
   std::vector<mprof_ctx*> cs;
   for (auto& kv : by_device) cs.push_back(kv.second);
@@ -961,11 +982,15 @@ void trim_ctx(mprof_ctx* c) {
   cudaStreamSynchronize(c->stream);
   cudaFree(c->ws);
   cudaFree(c->io);
-  cudaFree(c->tiles_d);
+  for (auto& sl : c->tile_slot) {
+    cudaFree(sl.d);
+    sl.d = nullptr;
+    sl.cap = 0;
+    std::fill(sl.key, sl.key + 9, -1LL);
+    std::vector<int4>().swap(sl.h);
+  }
   c->ws = c->io = nullptr;
-  c->tiles_d = nullptr;
-  c->ws_bytes = c->io_bytes = c->tiles_cap = 0;
-  std::fill(c->tiles_key, c->tiles_key + 9, -1LL);
+  c->ws_bytes = c->io_bytes = 0;
   c->stats_t = nullptr;
 }
 
@@ -1241,20 +1266,32 @@ long long choose_R(const mprof_config* cfg, const Grid& gx, int slots) {
 int32_t build_tiles(mprof_ctx* c, const Grid& g, long long k_lo, long long k_hi, long long R,
                     long long l_old, long long* ntiles) {
   const long long key[9] = {g.L, k_lo, k_hi, R, g.exact ? -g.g0 : g.g0, g.row_hi, g.m, g.S, l_old};
-  if (std::equal(key, key + 9, c->tiles_key)) {
-    *ntiles = (long long)c->tiles_h.size();
-    return MPROF_OK;
+  mprof_ctx::TileSlot* lru = &c->tile_slot[0];
+  for (auto& sl : c->tile_slot) {
+    if (std::equal(key, key + 9, sl.key)) {
+      sl.used = ++c->tile_clock;
+      c->tiles = &sl;
+      *ntiles = (long long)sl.h.size();
+      return MPROF_OK;
+    }
+    if (sl.used < lru->used) lru = &sl;
   }
-  tile_list(g, k_lo, k_hi, R, c->tiles_h, nullptr, l_old);
-  const size_t need = c->tiles_h.size() * sizeof(int4);
-  void* p = c->tiles_d;
-  int32_t st = ensure(&p, &c->tiles_cap, std::max<size_t>(need, 16));
-  c->tiles_d = static_cast<int4*>(p);
+  // replace the least recently used table (stream-ordered upload: kernels still reading the old
+  // table of this slot were enqueued earlier on the same stream; ensure()'s cudaFree synchronizes)
+  mprof_ctx::TileSlot& sl = *lru;
+  std::fill(sl.key, sl.key + 9, -1LL);
+  tile_list(g, k_lo, k_hi, R, sl.h, nullptr, l_old);
+  const size_t need = sl.h.size() * sizeof(int4);
+  void* p = sl.d;
+  int32_t st = ensure(&p, &sl.cap, std::max<size_t>(need, 16));
+  sl.d = static_cast<int4*>(p);
   if (st != MPROF_OK) return st;
-  CK(cudaMemcpyAsync(c->tiles_d, c->tiles_h.data(), need, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaStreamSynchronize(c->stream));  // tiles_h may be rebuilt by the next call
-  std::copy(key, key + 9, c->tiles_key);
-  *ntiles = (long long)c->tiles_h.size();
+  CK(cudaMemcpyAsync(sl.d, sl.h.data(), need, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // the pageable host table may be rebuilt by a later call
+  std::copy(key, key + 9, sl.key);
+  sl.used = ++c->tile_clock;
+  c->tiles = &sl;
+  *ntiles = (long long)sl.h.size();
   return MPROF_OK;
 }
 
@@ -1704,13 +1741,17 @@ int32_t plan_series(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
                             ((long long)cfg->family << 8) | (cfg->precision << 4) | (c->zn_colscale ? 1 : 0) |
                                 (c->aamp_cov ? 2 : 0) | (c->wide ? 4 : 0) | (c->dense ? 8 : 0),
                             pbits, slots};
-  if (std::equal(key, key + 9, c->R_key)) {
-    out->R = c->R_val;
-  } else {
+  out->R = 0;
+  for (const auto& rc : c->R_cache)
+    if (std::equal(key, key + 9, rc.key)) out->R = rc.R;
+  if (!out->R) {
     out->R = choose_R(cfg, g, slots);
     if (!knobs().rows_per_tile) {
-      std::copy(key, key + 9, c->R_key);
-      c->R_val = out->R;
+      if (c->R_cache.size() >= 16) c->R_cache.erase(c->R_cache.begin());
+      mprof_ctx::RChoice rc;
+      std::copy(key, key + 9, rc.key);
+      rc.R = out->R;
+      c->R_cache.push_back(rc);
     }
   }
   c->plan_R = out->R;
@@ -1742,7 +1783,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   out->R = R;
   int32_t st = build_tiles(c, g, k_tile, k_hi, R, l_old, &out->ntiles);
   if (st != MPROF_OK) return st;
-  prm.tiles = c->tiles_d;
+  prm.tiles = c->tiles->d;
   prm.R = (int)std::min<long long>(R, INT_MAX);
   const bool want_stats = knobs().stats;
   if (want_stats) {
@@ -1754,7 +1795,7 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   const bool cov_main = (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale) ||
                         (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov);
   if (cov_main && !cfg->exact && !knobs().zn_no_near)  // the list is in ascending diagonal order
-    while (n_near < out->ntiles && c->tiles_h[n_near].x < g.g0 + kK) ++n_near;
+    while (n_near < out->ntiles && c->tiles->h[n_near].x < g.g0 + kK) ++n_near;
   st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
                       &out->ms);
   if (st != MPROF_OK) return st;
@@ -2004,7 +2045,8 @@ void mprof_ctx_destroy(mprof_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->ws) cudaFree(c->ws);
   if (c->io) cudaFree(c->io);
-  if (c->tiles_d) cudaFree(c->tiles_d);
+  for (auto& sl : c->tile_slot)
+    if (sl.d) cudaFree(sl.d);
   if (c->d_spread) cudaFree(c->d_spread);
   if (c->probe_d) cudaFree(c->probe_d);
   if (c->probe_cnt) cudaFree(c->probe_cnt);
@@ -2563,7 +2605,7 @@ int32_t mprof_state_extend(mprof_state* S, const double* samples, uint64_t count
   // cells swept: the tiles' cells (incremental) or the whole extended series
   uint64_t cells = 0;
   if (incremental) {
-    for (const int4& tl : c->tiles_h)
+    for (const int4& tl : c->tiles->h)
       cells += (uint64_t)tile_cells(L_new, tl.x, tl.w, L_new, tl.y, tl.z - tl.y);
   } else {
     cells = mprof_band_cells(n_new, cfg->m, cfg->exclusion, (uint64_t)L_new);
@@ -2674,10 +2716,8 @@ int32_t mprof_ctx_set_progress(mprof_ctx* in, mprof_progress_fn fn, void* user) 
 
 void mprof_plan_destroy(mprof_plan* P) {
   if (!P) return;
-  if (P->ctx) {
-    cudaSetDevice(P->ctx->device);
-    cudaStreamSynchronize(P->ctx->stream);
-  }
+  // the context may already be gone (it is borrowed): cudaFree itself waits for the device
+  cudaSetDevice(P->device);
   cudaFree(P->ws);
   cudaFree(P->tiles);
   delete P;
@@ -2698,6 +2738,7 @@ int32_t mprof_plan_create(mprof_ctx* in, const double* d_t, uint64_t n64, const 
   const int n = (int)n64, L = n - (int)cfg->m + 1;
   mprof_plan* P = new mprof_plan();
   P->ctx = c;
+  P->device = c->device;
   P->t = d_t;
   P->n = n64;
   P->cfg = *cfg;
@@ -2802,7 +2843,7 @@ int32_t mprof_ctx_set_form(mprof_ctx* in, int32_t form) {
   int32_t st = resolve_ctx(in, &c);
   if (st != MPROF_OK) return st;
   c->form = form;
-  c->R_key[0] = -1;  // the rows-per-tile cache is keyed on the form flags, not the override
+  c->R_cache.clear();  // keyed on the form flags, not on the override
   return MPROF_OK;
 }
 

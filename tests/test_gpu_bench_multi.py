@@ -24,8 +24,8 @@ def free_port():
 def test_bench_two_ranks_on_one_gpu():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(ROOT / "bench.py"),
-           "--gpus", "2", "--share-gpu", "--steps", "2", "--warmup", "1", "--n", "65536",
-           "--m", "256", "--no-cpu-baseline", "--no-configs"]
+           "--gpus", "2", "--share-gpu", "--steps", "2", "--warmup", "1", "--series-len", "65536",
+           "--window", "256", "--no-cpu-baseline", "--no-configs"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]

@@ -3,7 +3,7 @@
 #   bash tools/capture_r01.sh <tag>      (tag e.g. r01_v14)
 TAG=${1:-r01_v14}
 set -x
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 2700 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench.err || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_l.log 2>&1
 python tools/time_c4.py C4aamp > /dev/null && ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:sweep_kernel<mpg::Wide<mpg::EuclidCov' -c 1 -o gpurun_out/aamp python tools/time_c4.py C4aamp > gpurun_out/ncu_a.log 2>&1

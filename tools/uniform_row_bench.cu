@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps)
         for (int d = 0; d < D; ++d) {
           const double2 cc = c[(d + u) % D];
           acc[d] = fma(rr.y, cc.x, fma(rr.x, cc.y, acc[d]));
-          if (KEYS == 1 || KEYS == 5 || ((KEYS == 2 || KEYS == 6) && (u == 3 || u == 7))) hb = max(hb, __double2hiint(acc[d]));
+          if (KEYS == 1 || KEYS == 5 || ((KEYS == 2 || KEYS == 6) && (u == 3 || u == 7)) || ((KEYS == 8 || KEYS == 9) && u == 7)) hb = max(hb, __double2hiint(acc[d]));
           if (KEYS == 3) hf = fmaxf(hf, __int_as_float(__double2hiint(acc[d])));
           if (KEYS == 4) { unsigned long long w = hp; int lo = (int)(unsigned)w; lo = max(lo, __double2hiint(acc[d])); hp = (w & 0xffffffff00000000ull) | (unsigned)lo; }
         }
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps)
       if (KEYS == 4) hb = (int)(unsigned)hp;
       if (KEYS == 7) hb = __double2hiint(acc[0]);
       hg = max(hg, hb - 0x100 * (s & 7));   // stand-in for a per-block threshold
-      if (KEYS && KEYS != 5 && KEYS != 6 && ((s / D) % G) == G - 1) { if (LAG) { if (prevhit) out[1] = s; prevhit = hg >= 0x7ff00000; } else if (hg >= 0x7ff00000) out[1] = s; hg = INT_MIN; }   // block hit test + branch, never taken
+      if (KEYS && KEYS != 5 && KEYS != 6 && KEYS != 9 && ((s / D) % G) == G - 1) { if (LAG) { if (prevhit) out[1] = s; prevhit = hg >= 0x7ff00000; } else if (hg >= 0x7ff00000) out[1] = s; hg = INT_MIN; }   // block hit test + branch, never taken
     }
   }
   int s = hm;
@@ -74,6 +74,18 @@ int main() {
   run<1, 1, 1, true>("const keys G1 lag", out, in);
   run<1, 1, 2, true>("const keys G2 lag", out, in);
   run<1, 2, 1, true>("const keys@3,7 G1 lag", out, in);
+  run<0, 0, 1>("smem nokeys", out, in);
+  run<1, 0, 1>("const nokeys", out, in);
+  run<0, 1, 8>("smem keys G8", out, in);
+  run<1, 1, 8>("const keys G8", out, in);
+  run<0, 2, 8>("smem keys@3,7 G8", out, in);
+  run<1, 2, 8>("const keys@3,7 G8", out, in);
+  run<0, 6, 1>("smem keys@3,7 nobranch", out, in);
+  run<1, 6, 1>("const keys@3,7 nobranch", out, in);
+  run<0, 8, 8>("smem keys@7 G8", out, in);
+  run<1, 8, 8>("const keys@7 G8", out, in);
+  run<0, 9, 1>("smem keys@7 nobranch", out, in);
+  run<1, 9, 1>("const keys@7 nobranch", out, in);
   }
   return 0;
 }
