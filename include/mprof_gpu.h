@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MPROF_GPU_ABI_VERSION 2
+#define MPROF_GPU_ABI_VERSION 3
 
 /* Status codes. 1..13 are mprof::ErrorCode + 1 in declaration order
  * (/root/reference/proj/include/mprof/core.hpp:16-30); >= 100 are device-side failures. */
@@ -103,6 +103,9 @@ typedef struct mprof_run_info {
    * 0 / 0 when no probe ran */
   uint32_t probe_replays;
   uint64_t probe_cells;
+  /* window launches of the constant-row kernel (0: the sweep ran the legacy tile kernel only) */
+  uint32_t row_windows;
+  uint32_t reserved;
 } mprof_run_info;
 
 typedef struct mprof_ctx mprof_ctx;
@@ -148,6 +151,12 @@ int32_t mprof_ctx_set_progress(mprof_ctx* ctx, mprof_progress_fn fn, void* user)
 enum { MPROF_FORM_AUTO = 0, MPROF_FORM_COV = 1, MPROF_FORM_WIDE = 2, MPROF_FORM_ALT = 3,
        MPROF_FORM_DENSE = 4 };
 int32_t mprof_ctx_set_form(mprof_ctx* ctx, int32_t form);
+/* Constant-row sweep (default on): the FP64 covariance-only forms (EuclidCov, Znorm<0>, Wide<...>)
+ * run as a sequence of row-window launches (1920 rows each) with the row operands passed as kernel
+ * parameters, i.e. in the constant bank (uniform-register DFMA operands); 0 keeps the
+ * single-launch tile kernel. Both paths do the same arithmetic per cell: identical P and I
+ * (tests/test_gpu_rowconst.py). Anytime sweeps (a progress observer) use the tile kernel. */
+int32_t mprof_ctx_set_row_const(mprof_ctx* ctx, int32_t enabled);
 
 /* ---- reference entry points (host buffers) ------------------------------------------------ */
 /* P[L] and I[L], L = n - m + 1, caller-allocated. `threads` (reference: CPU workers) selects

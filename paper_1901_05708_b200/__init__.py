@@ -223,7 +223,8 @@ class RunInfo(C.Structure):
                 ("sweep_ms", C.c_float), ("fp64_ops_per_cell", C.c_float),
                 ("fp32_ops_per_cell", C.c_float), ("_policy", C.c_char * 32),
                 ("hit_group", C.c_int32), ("probe_replays", C.c_uint32),
-                ("probe_cells", C.c_uint64)]
+                ("probe_cells", C.c_uint64), ("row_windows", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
     @property
     def policy(self) -> str:
@@ -280,6 +281,7 @@ EXPORTS = {
     "mprof_state_tail": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "mprof_ctx_set_progress": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "mprof_ctx_set_form": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "mprof_ctx_set_row_const": (C.c_int32, [C.c_void_p, C.c_int32]),
     "mprof_plan_create": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(_Config),
                                       C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p)]),
     "mprof_plan_sweep": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(RunInfo)]),
@@ -382,6 +384,10 @@ class Context:
     def set_form(self, form: "Form") -> None:
         """Filter form of FP64 fast-mode Euclidean / z-norm sweeps (mprof_ctx_set_form)."""
         _raise(lib().mprof_ctx_set_form(self.handle, int(form)))
+
+    def set_row_const(self, on: bool) -> None:
+        """Constant-row sweep of the covariance-only forms (mprof_ctx_set_row_const); on by default."""
+        _raise(lib().mprof_ctx_set_row_const(self.handle, 1 if on else 0))
 
     def close(self) -> None:
         if self.handle:

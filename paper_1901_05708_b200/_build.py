@@ -54,15 +54,20 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
     objdir = ROOT / "build" / "obj"
     objdir.mkdir(parents=True, exist_ok=True)
     objs = []
+    jobs = []
     for src in _sources():
         obj = objdir / (src.name + ".o")
         cmd = [NVCC, *NVFLAGS, *ARCH, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        r = _run(cmd)
-        if verbose:
-            print(r.stderr)
+        jobs.append(cmd)
         objs.append(str(obj))
+    # the translation units are independent: compile them side by side
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(4, len(jobs))) as pool:
+        for r in pool.map(_run, jobs):
+            if verbose:
+                print(r.stderr)
     tmp = LIB.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"])
     os.replace(tmp, LIB)

@@ -25,6 +25,7 @@
 
 #include "../../include/mprof_gpu.h"
 #include "sweep.cuh"
+#include "sweep_rc.h"
 
 using namespace mpg;
 
@@ -841,10 +842,16 @@ struct mprof_ctx {
   // between engines or series shapes on one context (AAMP then ACAMP of the same series, the
   // usual host-API pattern) neither rebuild and re-upload the table nor rerun the schedule model.
   struct TileSlot {
-    std::vector<int4> h;  // (first diagonal, first row, row end, diagonal end)
+    // (first diagonal, first row, row end, diagonal end), arranged as [tiles of the global
+    // block next to the exclusion zone | other legacy-kernel tiles | constant-row tiles by
+    // (first row, first diagonal)]
+    std::vector<int4> h;
+    long long n_near = 0;             // side-kernel tiles (covariance forms)
+    long long n_legacy = 0;           // tiles the legacy kernel sweeps, n_near included
+    std::vector<mpg::RcBand> bands;   // row bands of the constant-row part (offsets into h)
     int4* d = nullptr;
     size_t cap = 0;
-    long long key[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+    long long key[10] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
     unsigned long long used = 0;
   };
   static constexpr int kTileSlots = 4;
@@ -856,6 +863,15 @@ struct mprof_ctx {
     long long R;
   };
   std::vector<RChoice> R_cache;
+  // constant-row sweep (sweep_rc.h): streams, events, accumulator carry; on by default
+  mpg::RcRes rc;
+  bool rowconst = true;
+  // pinned host copy of the operand pairs the window launches pass as kernel parameters, valid
+  // for operand generation rc_host_gen of device array rc_host_src (prepare_operands bumps op_gen)
+  double2* rc_host = nullptr;
+  size_t rc_host_cap = 0;
+  const double2* rc_host_src = nullptr;
+  unsigned long long rc_host_gen = 0, op_gen = 1;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
   const double* stats_t = nullptr;
   uint64_t stats_n = 0, stats_m = 0;
@@ -906,7 +922,10 @@ struct mprof_plan {
   long long k_lo = 0, k_hi = 0;  // admissible band
   void* ws = nullptr;            // owned workspace (operands, profile, scratch)
   int4* tiles = nullptr;         // owned tile table
-  long long ntiles = 0, n_near = 0, R = 0;
+  long long ntiles = 0, n_near = 0, n_legacy = 0, R = 0;
+  std::vector<mpg::RcBand> bands;  // constant-row part of the tile table
+  int rc_policy = -1;
+  double2* host_pairs = nullptr;   // owned pinned mirror of the operand pairs (constant-row sweep)
   bool aamp_cov = false, zn_colscale = false, wide = false, dense = false;
   unsigned long long probe_replays = 0;
   double probe_cells = 0.0;
@@ -986,9 +1005,14 @@ void trim_ctx(mprof_ctx* c) {
     cudaFree(sl.d);
     sl.d = nullptr;
     sl.cap = 0;
-    std::fill(sl.key, sl.key + 9, -1LL);
+    std::fill(sl.key, sl.key + 10, -1LL);
     std::vector<int4>().swap(sl.h);
   }
+  mpg::rc_release(c->rc);
+  if (c->rc_host) cudaFreeHost(c->rc_host);
+  c->rc_host = nullptr;
+  c->rc_host_cap = 0;
+  c->rc_host_src = nullptr;
   c->ws = c->io = nullptr;
   c->ws_bytes = c->io_bytes = 0;
   c->stats_t = nullptr;
@@ -1263,12 +1287,53 @@ long long choose_R(const mprof_config* cfg, const Grid& gx, int slots) {
   return R;
 }
 
+// Arranges a tile list (tile_list order: ascending first diagonal, then first row) for the sweep:
+// the tiles of the global block next to the exclusion zone first (n_near; the covariance forms
+// sweep them with their side kernel), and, for a constant-row sweep (rc), the full-width global
+// blocks' tiles last, sorted by (first row, first diagonal) and described as row bands: all tiles
+// of a band start at the same row, their row ends do not increase with the diagonal, so the tiles
+// that still have a row transition in window w are a prefix of count[w] tiles.
+void arrange_tiles(const Grid& g, bool near_block, bool rc, std::vector<int4>& h, long long* n_near,
+                   long long* n_legacy, std::vector<mpg::RcBand>* bands) {
+  *n_near = 0;
+  if (near_block)
+    while (*n_near < (long long)h.size() && h[*n_near].x < g.g0 + kK) ++*n_near;
+  *n_legacy = (long long)h.size();
+  bands->clear();
+  if (!rc) return;
+  auto full_width = [&](const int4& t) { return g.block_hi(t.x) - g.block_lo(t.x) == kK; };
+  auto mid = std::stable_partition(h.begin() + *n_near, h.end(),
+                                   [&](const int4& t) { return !full_width(t); });
+  *n_legacy = mid - h.begin();
+  std::sort(mid, h.end(), [](const int4& a, const int4& b) {
+    return a.y != b.y ? a.y < b.y : a.x < b.x;
+  });
+  for (size_t i = (size_t)*n_legacy; i < h.size();) {
+    size_t j = i;
+    while (j < h.size() && h[j].y == h[i].y) ++j;
+    mpg::RcBand bd;
+    bd.off = (int)i;
+    bd.ra = h[i].y;
+    bd.count.push_back((int)(j - i));  // window 0: every tile seeds (and merges its seed cells)
+    for (int w = 1;; ++w) {
+      const long long r0 = (long long)bd.ra + (long long)w * mpg::kRcW;
+      size_t cnt = 0;
+      while (i + cnt < j && (long long)h[i + cnt].z - 1 > r0) ++cnt;
+      if (cnt == 0) break;
+      bd.count.push_back((int)cnt);
+    }
+    bands->push_back(std::move(bd));
+    i = j;
+  }
+}
+
 int32_t build_tiles(mprof_ctx* c, const Grid& g, long long k_lo, long long k_hi, long long R,
-                    long long l_old, long long* ntiles) {
-  const long long key[9] = {g.L, k_lo, k_hi, R, g.exact ? -g.g0 : g.g0, g.row_hi, g.m, g.S, l_old};
+                    long long l_old, bool near_block, bool rc, long long* ntiles) {
+  const long long key[10] = {g.L, k_lo, k_hi, R, g.exact ? -g.g0 : g.g0, g.row_hi, g.m, g.S, l_old,
+                             (near_block ? 1 : 0) | (rc ? 2 : 0)};
   mprof_ctx::TileSlot* lru = &c->tile_slot[0];
   for (auto& sl : c->tile_slot) {
-    if (std::equal(key, key + 9, sl.key)) {
+    if (std::equal(key, key + 10, sl.key)) {
       sl.used = ++c->tile_clock;
       c->tiles = &sl;
       *ntiles = (long long)sl.h.size();
@@ -1279,8 +1344,9 @@ int32_t build_tiles(mprof_ctx* c, const Grid& g, long long k_lo, long long k_hi,
   // replace the least recently used table (stream-ordered upload: kernels still reading the old
   // table of this slot were enqueued earlier on the same stream; ensure()'s cudaFree synchronizes)
   mprof_ctx::TileSlot& sl = *lru;
-  std::fill(sl.key, sl.key + 9, -1LL);
+  std::fill(sl.key, sl.key + 10, -1LL);
   tile_list(g, k_lo, k_hi, R, sl.h, nullptr, l_old);
+  arrange_tiles(g, near_block, rc, sl.h, &sl.n_near, &sl.n_legacy, &sl.bands);
   const size_t need = sl.h.size() * sizeof(int4);
   void* p = sl.d;
   int32_t st = ensure(&p, &sl.cap, std::max<size_t>(need, 16));
@@ -1288,7 +1354,7 @@ int32_t build_tiles(mprof_ctx* c, const Grid& g, long long k_lo, long long k_hi,
   if (st != MPROF_OK) return st;
   CK(cudaMemcpyAsync(sl.d, sl.h.data(), need, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // the pageable host table may be rebuilt by a later call
-  std::copy(key, key + 9, sl.key);
+  std::copy(key, key + 10, sl.key);
   sl.used = ++c->tile_clock;
   c->tiles = &sl;
   *ntiles = (long long)sl.h.size();
@@ -1448,10 +1514,52 @@ int32_t probe_form(mprof_ctx* c, bool zn, const SweepParams& prm, int kb_lo, uin
   return MPROF_OK;
 }
 
+// The constant-row kernel of the sweep policy (sweep_rc.h), or -1: FP64 fast-mode covariance-only
+// forms whose rows per tile are whole windows.
+int rc_policy_of(const mprof_ctx* c, const mprof_config* cfg, long long R) {
+  // (anytime sweeps run many small chunks: the legacy kernel's single launch per chunk)
+  if (!c->rowconst || cfg->exact || cfg->precision != MPROF_FP64 || c->dense || c->progress) return -1;
+  if (R <= 0) return -1;
+  if (cfg->family == MPROF_ZNORMALIZED)
+    return c->zn_colscale ? -1 : (c->wide ? mpg::kRcWideZnorm : mpg::kRcZnorm);
+  const bool l2 = cfg->family == MPROF_EUCLIDEAN || (cfg->family == MPROF_PNORM && cfg->p == 2.0);
+  if (l2 && c->aamp_cov) return c->wide ? mpg::kRcWideEuclidCov : mpg::kRcEuclidCov;
+  return -1;
+}
+
+// Pinned host mirror of `pairs` (count entries), refreshed when the operands were rebuilt.
+int32_t rc_host_pairs(mprof_ctx* c, const double2* pairs, size_t count, const double2** out) {
+  if (c->rc_host_src != pairs || c->rc_host_gen != c->op_gen || c->rc_host_cap < count) {
+    if (c->rc_host_cap < count) {
+      if (c->rc_host) cudaFreeHost(c->rc_host);
+      c->rc_host = nullptr;
+      c->rc_host_cap = 0;
+      CK(cudaMallocHost(&c->rc_host, count * sizeof(double2)));
+      c->rc_host_cap = count;
+    }
+    CK(cudaMemcpyAsync(c->rc_host, pairs, count * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->rc_host_src = pairs;
+    c->rc_host_gen = c->op_gen;
+  }
+  *out = c->rc_host;
+  return MPROF_OK;
+}
+
+// Sweeps a tile table arranged by arrange_tiles: tiles [0, n_near) on the side stream with the
+// side kernel, [n_near, n_legacy) with the policy's legacy kernel, the row bands with the
+// constant-row kernel (rc_policy >= 0).
 int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
-                       long long ntiles, long long n_near, int k1, bool first_diag,
-                       uint32_t* launches, float* ms) {
+                       long long ntiles, long long n_near, long long n_legacy,
+                       const std::vector<mpg::RcBand>& bands, int rc_policy,
+                       const double2* host_pairs, int k1, bool first_diag, uint32_t* launches,
+                       float* ms, uint32_t* rc_launches) {
   int32_t st = MPROF_OK;
+  if (n_legacy < ntiles && !host_pairs) {  // before the timed region: the mirror needs a sync
+    if (rc_policy < 0 || bands.empty()) return fail(MPROF_E_CUDA, "internal: row bands without a kernel");
+    st = rc_host_pairs(c, mpg::rc_pairs(rc_policy, prm), (size_t)std::max(prm.L - 1, 1), &host_pairs);
+    if (st != MPROF_OK) return st;
+  }
   if (first_diag && !cfg->exact) {
     st = with_policy(c, cfg, [&]<class P>() { return launch_first_diag<P>(c, prm, k1, launches); });
     if (st != MPROF_OK) return st;
@@ -1473,10 +1581,19 @@ int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams&
     if (st != MPROF_OK) return st;
     CK(cudaEventRecord(c->ev_join, c->side));
   }
+  n_legacy = std::min(std::max(n_legacy, n_near), ntiles);
   st = with_policy(c, cfg, [&]<class P>() {
-    return launch_tiles<P>(prm, n_near, ntiles - n_near, c->stream, launches);
+    return launch_tiles<P>(prm, n_near, n_legacy - n_near, c->stream, launches);
   });
   if (st != MPROF_OK) return st;
+  if (n_legacy < ntiles) {
+    if (rc_policy < 0 || bands.empty()) return fail(MPROF_E_CUDA, "internal: row bands without a kernel");
+    uint32_t nl = 0;
+    const cudaError_t e = mpg::rc_sweep(rc_policy, prm, bands, c->rc, c->stream, host_pairs, &nl);
+    if (e != cudaSuccess) return cuda_fail(e, "constant-row sweep");
+    *launches += nl;
+    if (rc_launches) *rc_launches += nl;
+  }
   if (n_near > 0) CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   if (c->timing) {
     CK(cudaEventRecord(c->ev1, c->stream));
@@ -1541,6 +1658,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
   const int g = grid_for(L);
   int32_t st = MPROF_OK;
   const bool zn = cfg->family == MPROF_ZNORMALIZED;
+  ++c->op_gen;  // the operand arrays are rebuilt: host mirrors of them are stale
   if (zn) {
     c->stats_t = nullptr;  // force: the series bytes behind d_t may have changed
     st = ensure_znorm_stats(c, d_t, (uint64_t)n, cfg, w);
@@ -1621,6 +1739,7 @@ int32_t prepare_operands(mprof_ctx* c, const double* d_t, int n, const mprof_con
 struct SweepOut {
   float ms = 0.f;
   long long ntiles = 0, R = 0;
+  uint32_t rc_launches = 0;  // window launches of the constant-row kernel
 };
 
 SweepParams make_params(const mprof_ctx* c, const double* d_t, int n, const mprof_config* cfg,
@@ -1781,7 +1900,12 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
   SweepParams prm = make_params(c, d_t, n, cfg, w, k_hi, row_hi);
   const Grid g = grid_of(c, cfg, L, row_hi);
   out->R = R;
-  int32_t st = build_tiles(c, g, k_tile, k_hi, R, l_old, &out->ntiles);
+  // the global block next to the exclusion zone runs the side kernel (dispatch_sweep)
+  const bool cov_main = (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale) ||
+                        (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov);
+  const bool near_block = cov_main && !cfg->exact && !knobs().zn_no_near;
+  const int rc_policy = rc_policy_of(c, cfg, R);
+  int32_t st = build_tiles(c, g, k_tile, k_hi, R, l_old, near_block, rc_policy >= 0, &out->ntiles);
   if (st != MPROF_OK) return st;
   prm.tiles = c->tiles->d;
   prm.R = (int)std::min<long long>(R, INT_MAX);
@@ -1790,14 +1914,9 @@ int32_t sweep_tiles(mprof_ctx* c, const double* d_t, int n, const mprof_config* 
     CK(cudaMallocAsync(&prm.stats, 2 * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(prm.stats, 0, 2 * sizeof(unsigned long long), c->stream));
   }
-  // the global block next to the exclusion zone runs the side kernel (dispatch_sweep)
-  long long n_near = 0;
-  const bool cov_main = (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale) ||
-                        (cfg->family != MPROF_ZNORMALIZED && c->aamp_cov);
-  if (cov_main && !cfg->exact && !knobs().zn_no_near)  // the list is in ascending diagonal order
-    while (n_near < out->ntiles && c->tiles->h[n_near].x < g.g0 + kK) ++n_near;
-  st = dispatch_sweep(c, cfg, prm, out->ntiles, n_near, (int)cfg->exclusion, first_diag, launches,
-                      &out->ms);
+  st = dispatch_sweep(c, cfg, prm, out->ntiles, c->tiles->n_near, c->tiles->n_legacy,
+                      c->tiles->bands, rc_policy, nullptr, (int)cfg->exclusion, first_diag, launches,
+                      &out->ms, &out->rc_launches);
   if (st != MPROF_OK) return st;
   if (want_stats) {
     unsigned long long h[2];
@@ -1845,6 +1964,8 @@ void fill_info(mprof_ctx* c, const mprof_config* cfg, uint64_t cells, long long 
   info->tiles = (uint64_t)so.ntiles;
   info->rows_per_tile = (uint64_t)so.R;
   info->kernel_launches = launches;
+  info->row_windows = so.rc_launches;
+  info->reserved = 0;
   info->sweep_ms = so.ms;
   std::memset(info->policy, 0, sizeof info->policy);
   with_policy(c, cfg, [&]<class P>() {
@@ -1903,6 +2024,7 @@ int32_t sweep_impl(mprof_ctx* c, const double* d_t, uint64_t n64, const mprof_co
                        plan.R, 0, &launches, &part);
       if (st != MPROF_OK) return st;
       so.ms += part.ms;
+      so.rc_launches += part.rc_launches;
       so.ntiles += part.ntiles;
       so.R = part.R;
       CK(cudaStreamSynchronize(c->stream));
@@ -2047,6 +2169,8 @@ void mprof_ctx_destroy(mprof_ctx* c) {
   if (c->io) cudaFree(c->io);
   for (auto& sl : c->tile_slot)
     if (sl.d) cudaFree(sl.d);
+  mpg::rc_release(c->rc);
+  if (c->rc_host) cudaFreeHost(c->rc_host);
   if (c->d_spread) cudaFree(c->d_spread);
   if (c->probe_d) cudaFree(c->probe_d);
   if (c->probe_cnt) cudaFree(c->probe_cnt);
@@ -2720,6 +2844,7 @@ void mprof_plan_destroy(mprof_plan* P) {
   cudaSetDevice(P->device);
   cudaFree(P->ws);
   cudaFree(P->tiles);
+  if (P->host_pairs) cudaFreeHost(P->host_pairs);
   delete P;
 }
 
@@ -2778,8 +2903,20 @@ int32_t mprof_plan_create(mprof_ctx* in, const double* d_t, uint64_t n64, const 
     tile_list(g, k_tile, P->k_hi, P->R, tl, nullptr);
     P->ntiles = (long long)tl.size();
     const bool cov_main = zn ? !c->zn_colscale : c->aamp_cov;
-    if (cov_main && !cfg->exact && !knobs().zn_no_near)
-      while (P->n_near < P->ntiles && tl[P->n_near].x < g.g0 + kK) ++P->n_near;
+    P->rc_policy = rc_policy_of(c, cfg, P->R);
+    arrange_tiles(g, cov_main && !cfg->exact && !knobs().zn_no_near, P->rc_policy >= 0, tl,
+                  &P->n_near, &P->n_legacy, &P->bands);
+    if (!P->bands.empty()) {  // the window launches' row operands: one host mirror per plan
+      const SweepParams pp = make_params(c, d_t, n, cfg, w, L, L);
+      const size_t cnt = (size_t)std::max(L - 1, 1);
+      if (cudaMallocHost(&P->host_pairs, cnt * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(MPROF_E_OOM, "plan operand mirror"));
+      }
+      const cudaError_t e = cudaMemcpyAsync(P->host_pairs, mpg::rc_pairs(P->rc_policy, pp),
+                                            cnt * sizeof(double2), cudaMemcpyDeviceToHost, c->stream);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "plan operand mirror"));
+    }
     if (!tl.empty()) {
       if (cudaMalloc(&P->tiles, tl.size() * sizeof(int4)) != cudaSuccess) {
         cudaGetLastError();
@@ -2821,8 +2958,9 @@ int32_t mprof_plan_sweep(mprof_plan* P, double* d_cmp, int64_t* d_idx, mprof_run
     SweepParams prm = make_params(c, P->t, n, cfg, w, (int)P->k_hi, L);
     prm.tiles = P->tiles;
     prm.R = (int)std::min<long long>(P->R, INT_MAX);
-    int32_t st = dispatch_sweep(c, cfg, prm, P->ntiles, P->n_near, (int)cfg->exclusion, true,
-                                &launches, &so.ms);
+    int32_t st = dispatch_sweep(c, cfg, prm, P->ntiles, P->n_near, P->n_legacy, P->bands,
+                                P->rc_policy, P->host_pairs, (int)cfg->exclusion, true, &launches,
+                                &so.ms, &so.rc_launches);
     if (st != MPROF_OK) return st;
     if (zn) {
       st = flat_fix(c, w.B, L, (int)P->k_lo, (int)P->k_hi, w, w.best, &launches);
@@ -2844,6 +2982,14 @@ int32_t mprof_ctx_set_form(mprof_ctx* in, int32_t form) {
   if (st != MPROF_OK) return st;
   c->form = form;
   c->R_cache.clear();  // keyed on the form flags, not on the override
+  return MPROF_OK;
+}
+
+int32_t mprof_ctx_set_row_const(mprof_ctx* in, int32_t enabled) {
+  mprof_ctx* c = nullptr;
+  int32_t st = resolve_ctx(in, &c);
+  if (st != MPROF_OK) return st;
+  c->rowconst = enabled != 0;
   return MPROF_OK;
 }
 

@@ -709,7 +709,7 @@ struct Acc {
 // Exact merge of one flagged cell (rarely reached): column entry first, then the row candidate.
 // Positions (row, j) index the profile being swept; the stored neighbour indices are mapped by
 // out_index (identity except for reflected sweeps) so ties compare in original coordinates.
-__device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhit, int row, int j,
+static __device__ __noinline__ void merge_cell(double v, int h, bool rowhit, bool colhit, int row, int j,
                                         int* ct, BestEntry* best, unsigned long long* rv,
                                         int* rj, unsigned long long* stats) {
   MPG_CHECK(row >= 0 && j > row);
@@ -1450,7 +1450,7 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
 // Issue the cp.async copies of stage st (row transitions i0 .. i0+S-1, i0 = ra + st*S):
 // its row operands and thresholds, the thresholds of its whole live column window, and the
 // column operands that enter the ring with it (all NCOL for stage 0, S afterwards).
-template <class P, int D, int T, int S>
+template <class P, int D, int T, int S, bool ROWA = true>
 __device__ __forceinline__ void load_stage(SweepSmem<P, D, T, S>& sm, const SweepParams& prm,
                                            int st, int ra, int kb) {
   using G = Geo<D, T, S>;
@@ -1481,7 +1481,7 @@ __device__ __forceinline__ void load_stage(SweepSmem<P, D, T, S>& sm, const Swee
     const int pa = i0 + x;
     const int pb = pa + 1;
     const bool va = pa < L - 1, vb = pb < L;
-    cp_async<sizeof(V2)>(&sm.rowA[b][x], A + (va ? pa : 0), va);
+    if constexpr (ROWA) cp_async<sizeof(V2)>(&sm.rowA[b][x], A + (va ? pa : 0), va);
     if constexpr (P::kHasB) cp_async<sizeof(VB)>(&sm.rowB[b][x], Bs + (vb ? pb : 0), vb);
     cp_async<4>(&sm.rowT[b][x], bestw + 4 * (vb ? pb : 0) + 1, vb);
   }

@@ -1,0 +1,84 @@
+// sweep_rc.h — host interface of the constant-row sweep (csrc/sweep_rc.cu).
+//
+// The covariance-only FP64 sweeps (Znorm<0>, EuclidCov and their Wide<> forms) are bound by the
+// register-file reads of their DFMAs: with the row operand in a vector register every second DFMA
+// reads three 64-bit registers and dispatches in 3 cycles against its 2-cycle pipe slot
+// (DESIGN.md §4). The row operand is the same for every thread of the grid that works on the same
+// row, so this path puts it in the CONSTANT bank: the sweep runs as a sequence of row WINDOWS of
+// kRcW rows, one launch per window, whose row operands travel as a KERNEL PARAMETER (30 KB of the
+// 32 KB parameter space, bank 0; the host keeps a pinned copy of the operand array); the kernel
+// reads them with LDCU into uniform registers and its DFMAs take a uniform-register operand
+// (DFMA R, R, UR, R: two vector register reads). A tile (1024 diagonals x R rows, the legacy
+// kernel's CTA) becomes ceil(R / kRcW) consecutive window launches that carry their accumulators
+// through a global buffer; the tiles that start at the same row form a band whose windows are
+// chained on one stream, and the bands run concurrently on kRcChains streams (each launch has at
+// most L / 1024 CTAs: the chains fill each other's tails). Every cell keeps the arithmetic of the
+// legacy kernel (same seeds on the same row grid, same slide order), so the two paths give
+// bit-identical profiles (tests/test_gpu_rowconst.py).
+// (A __constant__ array refilled by stream-ordered device copies was measured first: 64 KB hold
+// only 2 x 2048 or 8 x 512 rows, i.e. few chains or short windows: C4 AAMP 114.7 / 102.5 ms.)
+//
+// Reference hot loop replaced: EuclidScan / ZnormScan driven by scan_diagonals
+// (/root/reference/proj/src/diag_scan.cpp:7-85, src/detail/diag_scan.hpp:193-259).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "sweep.cuh"
+
+namespace mpg {
+
+// Rows per window (operand pairs of 16 bytes in the kernel parameter space, which holds 32 764
+// bytes in all) and concurrent band chains (streams).
+#ifndef MPROF_RC_W
+#define MPROF_RC_W 1920
+#endif
+#ifndef MPROF_RC_CHAINS
+#define MPROF_RC_CHAINS 8
+#endif
+constexpr int kRcW = MPROF_RC_W;
+constexpr int kRcSlots = MPROF_RC_CHAINS;
+static_assert(kRcW * 16 <= 30720, "the row window must fit the kernel parameter space");
+
+enum RcPolicy { kRcZnorm = 0, kRcWideZnorm = 1, kRcEuclidCov = 2, kRcWideEuclidCov = 3 };
+
+// One row band of the tile grid: the tiles that start at row `ra` (ascending first diagonal, so
+// their row ends are non-increasing and the tiles still alive in window w are a prefix), at
+// offset `off` of the device tile table; count[w] = tiles with a row transition in window w
+// (windows of kRcW rows from `ra`; count[0] = every tile: window 0 also merges the seed cells).
+struct RcBand {
+  int off = 0;
+  int ra = 0;
+  std::vector<int> count;
+};
+
+// Streams, events and the accumulator carry buffer of one context.
+struct RcRes {
+  cudaStream_t st[kRcSlots] = {};
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[kRcSlots] = {};
+  double* acc = nullptr;     // kRcSlots (chains) x acc_tiles x K doubles
+  size_t acc_tiles = 0;
+};
+
+// Rows per shared-memory stage of the policy's constant-row kernel.
+int rc_stage_rows(int policy);
+
+// Resident CTAs per SM of the policy's constant-row kernel.
+int rc_blocks_per_sm(int policy);
+
+// Sweeps the bands' tiles (prm.tiles = device table the band offsets index) with the constant-row
+// kernel of `policy`: window launches chained per band on the context's chain streams, forked
+// from and joined to `main`. host_pairs = host copy of the policy's operand pairs (prm.A, or
+// prm.A2 for the covariance-form AAMP), L - 1 entries. Adds the kernel launches to *launches.
+cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBand>& bands,
+                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches);
+
+// Device pointer of the policy's operand pairs in prm (what host_pairs must mirror).
+const double2* rc_pairs(int policy, const SweepParams& prm);
+
+void rc_release(RcRes& res);
+
+}  // namespace mpg

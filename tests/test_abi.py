@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol(mp):
 
 def test_abi_version_and_strings(mp):
     L = mp.lib()
-    assert L.mprof_abi_version() == 2
+    assert L.mprof_abi_version() == 3
     assert L.mprof_status_string(0) == b"ok"
     assert L.mprof_status_string(9) == b"BadKind"
     assert L.mprof_status_string(100) == b"Cuda"

@@ -1,0 +1,67 @@
+"""Constant-row sweep (csrc/sweep_rc.cu) against the legacy tile kernel: the two paths do the same
+arithmetic per cell (same seeds on the same row grid, same slide order), so P and I must be
+bit-identical; the run info says which path ran. Series: a C4 prefix (n = 2^18, m = 1024: large
+enough for the form probe)."""
+import numpy as np
+import pytest
+
+import paper_1901_05708_b200 as mp
+from paper_1901_05708_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+N, M = 1 << 18, 1024
+
+
+@pytest.fixture(scope="module")
+def series():
+    return W.c4(n=N)
+
+
+def run(series, family, form, excl, row_const, k_lo=0, k_hi=0):
+    ctx = mp.Context(0)
+    ctx.set_form(form)
+    ctx.set_row_const(row_const)
+    kind = mp.DistanceKind.euclidean() if family == "aamp" else mp.DistanceKind.znormalized()
+    cfg = mp.ProfileConfig(M, kind)
+    cfg.exclusion = excl
+    fn = mp.aamp if family == "aamp" else mp.acamp
+    r = fn(mp.make_time_series(series), cfg, ctx=ctx)
+    ctx.close()
+    return r
+
+
+@pytest.mark.parametrize("family", ["aamp", "acamp"])
+@pytest.mark.parametrize("form", [mp.Form.Wide, mp.Form.Cov])
+@pytest.mark.parametrize("excl", [1, M])
+def test_row_const_bit_identical_to_tile_kernel(series, family, form, excl):
+    a = run(series, family, form, excl, True)
+    b = run(series, family, form, excl, False)
+    assert a.info.row_windows > 0 and b.info.row_windows == 0
+    assert a.info.policy == b.info.policy
+    assert a.info.rows_per_tile == b.info.rows_per_tile
+    np.testing.assert_array_equal(a.nn_index, b.nn_index)
+    np.testing.assert_array_equal(a.distances.view(np.uint64), b.distances.view(np.uint64))
+
+
+def test_row_const_is_the_default_where_it_applies(series):
+    ctx = mp.Context(0)
+    cfg = mp.ProfileConfig(M, mp.DistanceKind.znormalized())
+    r = mp.acamp(mp.make_time_series(series), cfg, ctx=ctx)
+    assert r.info.policy in ("Wide<Znorm<0>>", "Znorm<0>") and r.info.row_windows > 0
+    # column-scaled form, p-norm and small sweeps keep the tile kernel
+    ctx.set_form(mp.Form.Alt)
+    r = mp.acamp(mp.make_time_series(series), cfg, ctx=ctx)
+    assert r.info.policy == "Znorm<1>" and r.info.row_windows == 0
+    ctx.close()
+
+
+def test_row_const_bands_merge_to_the_single_sweep(series):
+    """Diagonal bands (the multi-GPU split) through the constant-row kernel merge to the profile of
+    one sweep, bit-identically (band edges cut tiles: the guarded stage variant runs)."""
+    cfg = mp.ProfileConfig(M, mp.DistanceKind.euclidean())
+    whole = mp.profile_multi(mp.make_time_series(series), cfg, [0], "aamp")
+    parts = mp.profile_multi(mp.make_time_series(series), cfg, [0, 0, 0], "aamp")
+    assert whole.info.row_windows > 0
+    np.testing.assert_array_equal(whole.nn_index, parts.nn_index)
+    np.testing.assert_array_equal(whole.distances.view(np.uint64), parts.distances.view(np.uint64))

@@ -1,0 +1,113 @@
+// Inner-loop microbenchmark for the constant-bank row operand design (experiments only):
+// row operands from __constant__ (LDCU -> uniform registers, DFMA R, R, UR, R), a branch-free
+// group loop with a deferred hit mask per stage, group-start accumulators stashed in shared
+// memory, per-block float thresholds from shared tables. Variants: KEYS (1 all sub-steps, 2 sub-steps
+// 3 and 7, 3 sub-step 7), SRC (0 shared rows, 1 constant rows), BR (0 deferred mask, 1 branch per
+// group), dynamic shared memory to cap the CTAs per SM.
+#include <cstdio>
+#include <climits>
+#include <cuda_runtime.h>
+constexpr int D = 8, T = 128, S = 128, HG = 8, NSTAGE = 4;
+constexpr int NS = S * NSTAGE;
+__constant__ double2 crow[NS];
+template <int SRC, int KEYS, int BR>
+__global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps) {
+  extern __shared__ unsigned char dyn[];
+  __shared__ double2 col[(NS + T * D + 2 * D) * 9 / 8 + 8];
+  __shared__ double2 row[SRC == 0 ? NS : 1];
+  __shared__ float2 zrow[NS / D], zcol[(NS + T * D) / D + 2];
+  __shared__ double stash[S / (HG * D)][D][T];
+  for (int i = threadIdx.x; i < (NS + T * D + 2 * D) * 9 / 8 + 8; i += T) col[i] = in[i % 4096];
+  if (SRC == 0) for (int i = threadIdx.x; i < NS; i += T) row[i] = in[(i * 7) % 4096];
+  for (int i = threadIdx.x; i < NS / D; i += T) zrow[i] = make_float2(1e30f, 1.f);
+  for (int i = threadIdx.x; i < (NS + T * D) / D + 2; i += T) zcol[i] = make_float2(1e30f, 1.f);
+  if (threadIdx.x == 0 && reps < 0) dyn[0] = 1;
+  __syncthreads();
+  double acc[D]; double2 c[D];
+  const int xb = threadIdx.x * D;
+#pragma unroll
+  for (int d = 0; d < D; ++d) { acc[d] = 0.0; c[d] = col[(xb + d) + (xb + d) / D]; }
+  for (int r = 0; r < reps; ++r) {
+    // per-thread addressing is kept on bumped pointers so that the loop counters stay uniform
+    // (ptxas then loads the constant rows with LDCU into uniform registers)
+    const float2* zcp = zcol + threadIdx.x;
+    const double2* colp = col + (xb + D) + (xb + D) / D;
+#pragma unroll 1
+    for (int st = 0; st < NSTAGE; ++st) {
+      unsigned mask = 0;
+#pragma unroll 1
+      for (int s0 = st * S; s0 < (st + 1) * S; s0 += HG * D) {
+        const int gi = (s0 - st * S) / (HG * D);
+#pragma unroll
+        for (int d = 0; d < D; ++d) stash[gi][d][threadIdx.x] = acc[d];
+        bool hit = false;
+        const float2* zc = zcp; zcp += HG;
+        const double2* cp = colp; colp += HG * (D + 1);
+#pragma unroll
+        for (int g = 0; g < HG; ++g) {
+          const int s = s0 + g * D;
+          const float2 rq = zrow[s / D], cq = zc[g];
+          const float th = fminf(__fmul_rd(rq.x, cq.y), __fmul_rd(cq.x, rq.y));
+          const int theta = th > 0.f ? __double2hiint((double)th) : INT_MIN;
+          int hb = INT_MIN;
+#pragma unroll
+          for (int u = 0; u < D; ++u) {
+            const double2 rr = SRC == 0 ? row[s + u] : crow[s + u];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+              const double2 cc = c[(d + u) % D];
+              acc[d] = fma(rr.y, cc.x, fma(rr.x, cc.y, acc[d]));
+              if (KEYS == 1 || (KEYS == 2 && (u == 3 || u == 7)) || (KEYS == 3 && u == 7))
+                hb = max(hb, __double2hiint(acc[d]));
+            }
+            c[u] = cp[g * (D + 1) + u];
+          }
+          hit |= hb >= theta;
+        }
+        if (BR == 1) { if (hit) out[1] = s0; }
+        else mask |= (hit ? 1u : 0u) << gi;
+      }
+      if (BR == 0 && mask) out[1] = mask;
+      __syncthreads();
+    }
+  }
+  int s = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) s ^= __double2hiint(acc[d]);
+  if (s == 12345) out[0] = s;
+}
+template <int SRC, int KEYS, int BR>
+void run(const char* name, int* out, const double2* in, int dynsmem) {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  auto kern = k<SRC, KEYS, BR>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dynsmem);
+  int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, dynsmem);
+  const int blocks = sms * 12 * 4, reps = 64;
+  kern<<<blocks, T, dynsmem>>>(out, in, 1);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kern<<<blocks, T, dynsmem>>>(out, in, reps);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  const double cells = (double)blocks * T * D * NS * reps;
+  printf("%-34s occ %d %8.3f ms  %6.3f Tcells/s  FP64 pipe %5.1f%%  err=%s\n", name, occ, ms,
+         cells / (ms * 1e-3) / 1e12, 100.0 * cells * 2.0 / (ms * 1e-3) / (sms * 64 * 1.965e9),
+         cudaGetErrorString(cudaGetLastError()));
+}
+int main() {
+  int* out; double2* in;
+  cudaMalloc(&out, 8); cudaMalloc(&in, 4096 * 16); cudaMemset(in, 0, 4096 * 16);
+  double2 h[NS]; for (int i = 0; i < NS; ++i) h[i] = make_double2(1e-3 * i, 2e-3 * i);
+  cudaMemcpyToSymbol(crow, h, sizeof(h));
+  for (int dyn : {0, 20 << 10, 40 << 10}) {
+    run<0, 1, 1>("smem keys branch/group", out, in, dyn);
+    run<0, 1, 0>("smem keys deferred", out, in, dyn);
+    run<1, 1, 1>("const keys branch/group", out, in, dyn);
+    run<1, 1, 0>("const keys deferred", out, in, dyn);
+    run<1, 2, 0>("const keys@3,7 deferred", out, in, dyn);
+    run<1, 3, 0>("const keys@7 deferred", out, in, dyn);
+    run<0, 2, 0>("smem keys@3,7 deferred", out, in, dyn);
+    run<0, 3, 0>("smem keys@7 deferred", out, in, dyn);
+  }
+  return 0;
+}

@@ -7,9 +7,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1901_05708_b200 as mp  # noqa: E402
 from paper_1901_05708_b200 import workloads as W  # noqa: E402
 
-names = sys.argv[1:] or ["C4aamp", "C4acamp"]
+args = [a for a in sys.argv[1:] if a != "norc"]
+names = args or ["C4aamp", "C4acamp"]
 ctx = mp.Context(0)
 ctx.set_timing(True)
+if "norc" in sys.argv[1:]:
+    ctx.set_row_const(False)  # the legacy single-launch tile kernel
 out = {}
 for name in names:
     c = W.CONFIGS[name]
@@ -26,6 +29,6 @@ for name in names:
     best = min(ms[1:])
     out[name] = {"sweep_ms": round(best, 3), "cells_per_s": f"{res.info.cells / (best * 1e-3):.4e}",
                  "tiles": res.info.tiles, "R": res.info.rows_per_tile,
-                 "policy": getattr(res.info, "policy", "?"), "hg": getattr(res.info, "hit_group", 0),
+                 "policy": getattr(res.info, "policy", "?"), "row_windows": res.info.row_windows, "hg": getattr(res.info, "hit_group", 0),
                  "probe": [getattr(res.info, "probe_replays", 0), getattr(res.info, "probe_cells", 0)]}
 print(json.dumps(out))

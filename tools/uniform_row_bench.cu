@@ -3,8 +3,9 @@
 #include <cuda_runtime.h>
 constexpr int D = 8, T = 128, NS = 512;
 __constant__ double2 crow[NS];
-template <int SRC, int KEYS, int G = 1, bool LAG = false>
+template <int SRC, int KEYSV, int G = 1, bool LAG = false>
 __global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps) {
+  constexpr int KEYS = KEYSV % 100; constexpr bool VOTE = KEYSV >= 100;
   __shared__ double2 col[(NS + T * D + 2 * D) * 9 / 8 + 8];
   __shared__ double2 row[NS];
   for (int i = threadIdx.x; i < (NS + T * D + 2 * D) * 9 / 8 + 8; i += T) col[i] = in[i % 4096];
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps)
       if (KEYS == 4) hb = (int)(unsigned)hp;
       if (KEYS == 7) hb = __double2hiint(acc[0]);
       hg = max(hg, hb - 0x100 * (s & 7));   // stand-in for a per-block threshold
-      if (KEYS && KEYS != 5 && KEYS != 6 && KEYS != 9 && ((s / D) % G) == G - 1) { if (LAG) { if (prevhit) out[1] = s; prevhit = hg >= 0x7ff00000; } else if (hg >= 0x7ff00000) out[1] = s; hg = INT_MIN; }   // block hit test + branch, never taken
+      if (KEYS && KEYS != 5 && KEYS != 6 && KEYS != 9 && ((s / D) % G) == G - 1) { if (LAG) { if (prevhit) out[1] = s; prevhit = hg >= 0x7ff00000; } else if (VOTE ? __any_sync(0xffffffffu, hg >= 0x7ff00000) : (hg >= 0x7ff00000)) out[1] = s; hg = INT_MIN; }   // block hit test + branch, never taken
     }
   }
   int s = hm;
@@ -65,7 +66,7 @@ int main() {
   cudaMalloc(&out, 8); cudaMalloc(&in, 4096 * 16); cudaMemset(in, 0, 4096 * 16);
   double2 h[NS]; for (int i = 0; i < NS; ++i) h[i] = make_double2(1e-3 * i, 2e-3 * i);
   cudaMemcpyToSymbol(crow, h, sizeof(h));
-  for (int rep = 0; rep < 2; ++rep) {
+  for (int rep = 0; rep < 1; ++rep) {
   run<0, 1, 1>("smem keys G1", out, in);
   run<0, 5, 1>("smem keys nobranch", out, in);
   run<0, 1, 1, true>("smem keys G1 lag", out, in);
@@ -74,6 +75,13 @@ int main() {
   run<1, 1, 1, true>("const keys G1 lag", out, in);
   run<1, 1, 2, true>("const keys G2 lag", out, in);
   run<1, 2, 1, true>("const keys@3,7 G1 lag", out, in);
+  run<0, 101, 8>("smem keys G8 vote", out, in);
+  run<1, 101, 8>("const keys G8 vote", out, in);
+  run<1, 101, 2>("const keys G2 vote", out, in);
+  run<1, 101, 1>("const keys G1 vote", out, in);
+  run<0, 102, 8>("smem keys@3,7 G8 vote", out, in);
+  run<1, 102, 8>("const keys@3,7 G8 vote", out, in);
+  run<1, 108, 8>("const keys@7 G8 vote", out, in);
   run<0, 0, 1>("smem nokeys", out, in);
   run<1, 0, 1>("const nokeys", out, in);
   run<0, 1, 8>("smem keys G8", out, in);
