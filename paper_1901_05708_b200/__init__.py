@@ -385,9 +385,10 @@ class Context:
         """Filter form of FP64 fast-mode Euclidean / z-norm sweeps (mprof_ctx_set_form)."""
         _raise(lib().mprof_ctx_set_form(self.handle, int(form)))
 
-    def set_row_const(self, on: bool) -> None:
-        """Constant-row sweep of the covariance-only forms (mprof_ctx_set_row_const); on by default."""
-        _raise(lib().mprof_ctx_set_row_const(self.handle, 1 if on else 0))
+    def set_row_const(self, on) -> None:
+        """Constant-row sweep (mprof_ctx_set_row_const): True / 1 (default) for the Wide<> forms,
+        2 for every covariance-only form, False / 0 off."""
+        _raise(lib().mprof_ctx_set_row_const(self.handle, int(on)))
 
     def close(self) -> None:
         if self.handle:

@@ -41,11 +41,22 @@ constexpr int rc_stage_rows_of() {
 
 // Shared memory of the constant-row kernel: the legacy layout plus the stash of the accumulators
 // at the start of every super-group of kRcSuper blocks (the deferred replays restart there).
-constexpr int kRcSuper = 8;  // blocks per stash
+#ifndef MPROF_RC_SUPER
+#define MPROF_RC_SUPER 8
+#endif
+constexpr int kRcSuper = MPROF_RC_SUPER;  // blocks per stash
+// MPROF_RC_STASH_GLOBAL = 1 keeps the stash in global memory instead (per resident CTA
+// S / 64 x 8 KB that stay in L2: 64 bytes stored per thread per 512 cells), which frees 16 KB of
+// shared memory per CTA.
+#ifndef MPROF_RC_STASH_GLOBAL
+#define MPROF_RC_STASH_GLOBAL 0
+#endif
+template <int D, int T, int S>
+constexpr int rc_stash_doubles() { return S / (kRcSuper * D) * D * T; }
 template <class P, int D, int T, int S>
 struct RcSmem {
   SweepSmem<P, D, T, S> base;
-  double stash[S / (kRcSuper * D)][D][T];
+  double stash[MPROF_RC_STASH_GLOBAL ? 1 : rc_stash_doubles<D, T, S>()];  // [super-group][d][thread]
 };
 
 // The slide of one block without any cell test (bit-identical to the hot loop's and to
@@ -90,7 +101,8 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
                                              typename P::V (&acc)[D], int i0, int cnt, int kt,
                                              int kend, int L, BestEntry* best, double p,
                                              unsigned long long* stats, const double2* crow,
-                                             int& ci, const typename P::V2* rowA_g, int svz) {
+                                             int& ci, const typename P::V2* rowA_g, int svz,
+                                             double* gstash) {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
   using SMT = SweepSmem<P, D, T, S>;
@@ -129,6 +141,7 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
   const float2* zct = &sm.zcol[EQ ? 0 : threadIdx.x];
   const float4* ert = &sm.erow[0];
   const float2* zrt = &sm.zrow[0];
+  double* stash = (MPROF_RC_STASH_GLOBAL ? gstash : rsm.stash) + threadIdx.x;
   unsigned hmask = 0;  // bit (sg * GPS + group): the group passed its block bounds
   int theta_nx;
   if constexpr (EQ) theta_nx = theta_e(ert[0], ect[0]);
@@ -138,7 +151,7 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
 #pragma unroll 1
   for (int s0 = 0; s0 < lim; s0 += kRcSuper * D, ++sg) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) rsm.stash[sg][d][threadIdx.x] = acc[d];
+    for (int d = 0; d < D; ++d) stash[(sg * D + d) * T] = acc[d];
 #pragma unroll
     for (int gg = 0; gg < GPS; ++gg) {
       bool hit = false;
@@ -201,7 +214,7 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
     }
     Acc<P, D> a0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) a0.a[d] = rsm.stash[g2][d][threadIdx.x];
+    for (int d = 0; d < D; ++d) a0.a[d] = stash[(g2 * D + d) * T];
 #pragma unroll 1
     for (int g = 0; g < kRcSuper; ++g) {
       if (GUARD && sv >= cnt) break;
@@ -250,7 +263,10 @@ __global__ void __launch_bounds__(T, MINB)
     if (threadIdx.x == 0) g_cell_ctx = CellCtx{prm.S, prm.mu, static_cast<double>(m)};
     __syncthreads();
   }
-  double* carry = rc.acc + (static_cast<size_t>(blockIdx.x) * G::K + threadIdx.x * D);
+  // per tile of the launch: [carry K | stash] doubles
+  constexpr int kPerTile = G::K + (MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<D, T, S>() : 0);
+  double* carry = rc.acc + (static_cast<size_t>(blockIdx.x) * kPerTile + threadIdx.x * D);
+  double* gstash = rc.acc + (static_cast<size_t>(blockIdx.x) * kPerTile + G::K);
   V acc[D];
   if (rc.w == 0) {
     // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d), as sweep_kernel ----
@@ -345,10 +361,10 @@ __global__ void __launch_bounds__(T, MINB)
     const bool full = (cnt == S) && (kb + G::K <= kend) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {
       run_stage_rc<P, D, T, S, false>(rsm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p,
-                                      prm.stats, rc.rows, ci, A + i0, rc.zero);
+                                      prm.stats, rc.rows, ci, A + i0, rc.zero, gstash);
     } else {
       run_stage_rc<P, D, T, S, true>(rsm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p,
-                                     prm.stats, rc.rows, ci, A + i0, rc.zero);
+                                     prm.stats, rc.rows, ci, A + i0, rc.zero, gstash);
     }
     if (st + 1 == nst) break;
     cp_async_wait<0>();
@@ -394,7 +410,7 @@ auto with_rc_policy(int policy, F&& f) {
 #endif
 }
 
-cudaError_t ensure_res(RcRes& res, size_t tiles) {
+cudaError_t ensure_res(RcRes& res, size_t tiles, size_t per_tile) {
   cudaError_t e;
   if (!res.fork) {
     if ((e = cudaEventCreateWithFlags(&res.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -403,12 +419,13 @@ cudaError_t ensure_res(RcRes& res, size_t tiles) {
       if ((e = cudaEventCreateWithFlags(&res.join[s], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
   }
-  if (tiles > res.acc_tiles) {
+  if (tiles * per_tile > res.acc_tiles * res.acc_per_tile || per_tile != res.acc_per_tile) {
     if (res.acc) cudaFree(res.acc);
     res.acc = nullptr;
     res.acc_tiles = 0;
-    if ((e = cudaMalloc(&res.acc, sizeof(double) * kD * kT * tiles * kRcSlots)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&res.acc, sizeof(double) * per_tile * tiles * kRcSlots)) != cudaSuccess) return e;
     res.acc_tiles = tiles;
+    res.acc_per_tile = per_tile;
   }
   return cudaSuccess;
 }
@@ -443,9 +460,10 @@ cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBan
   for (const RcBand& bd : bands)
     if (!bd.count.empty()) most = std::max<size_t>(most, (size_t)bd.count[0]);
   if (most == 0) return cudaSuccess;
-  cudaError_t e = ensure_res(res, most);
-  if (e != cudaSuccess) return e;
   return with_rc_policy(policy, [&]<class P>() -> cudaError_t {
+    constexpr size_t per_tile = (size_t)kD * kT + (MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<kD, kT, rc_stage_rows_of<P>()>() : 0);
+    cudaError_t e = ensure_res(res, most, per_tile);
+    if (e != cudaSuccess) return e;
     auto kern = rc_kernel<P>();
     const size_t smem = rc_smem<P>();
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -483,7 +501,7 @@ cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBan
         SweepParams q = prm;
         q.tiles = prm.tiles + bd.off;
         rc.w = w;
-        rc.acc = res.acc + (size_t)s * res.acc_tiles * kD * kT;
+        rc.acc = res.acc + (size_t)s * res.acc_tiles * per_tile;
         kern<<<(unsigned)nt, kT, smem, res.st[s]>>>(q, rc);
         if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
         ++*launches;

@@ -61,6 +61,7 @@ struct RcRes {
   cudaEvent_t join[kRcSlots] = {};
   double* acc = nullptr;     // kRcSlots (chains) x acc_tiles x K doubles
   size_t acc_tiles = 0;
+  size_t acc_per_tile = 0;   // doubles per tile: the carry (K) and, optionally, the replay stash
 };
 
 // Rows per shared-memory stage of the policy's constant-row kernel.

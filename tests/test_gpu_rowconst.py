@@ -21,7 +21,7 @@ def series():
 def run(series, family, form, excl, row_const, k_lo=0, k_hi=0):
     ctx = mp.Context(0)
     ctx.set_form(form)
-    ctx.set_row_const(row_const)
+    ctx.set_row_const(2 if row_const else 0)  # 2: also the non-Wide covariance-only forms
     kind = mp.DistanceKind.euclidean() if family == "aamp" else mp.DistanceKind.znormalized()
     cfg = mp.ProfileConfig(M, kind)
     cfg.exclusion = excl
