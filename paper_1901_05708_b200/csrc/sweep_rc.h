@@ -31,12 +31,15 @@
 namespace mpg {
 
 // Rows per window (operand pairs of 16 bytes in the kernel parameter space, which holds 32 764
-// bytes in all) and concurrent band chains (streams).
+// bytes in all; 1792 = 7 stages of 256 rows) and concurrent band chains (streams). Measured on C4
+// (sweep ms AAMP / ACAMP): 1920-row windows of 128-row stages, 8 chains 96.2 / 97.2, 16 chains
+// 95.0 / 96.3; 1792-row windows of 256-row stages (stash in global memory, 3 CTAs/SM), 8 chains
+// 91.7 / 92.4, 16 chains 90.0 / 91.5.
 #ifndef MPROF_RC_W
-#define MPROF_RC_W 1920
+#define MPROF_RC_W 1792
 #endif
 #ifndef MPROF_RC_CHAINS
-#define MPROF_RC_CHAINS 8
+#define MPROF_RC_CHAINS 16
 #endif
 constexpr int kRcW = MPROF_RC_W;
 constexpr int kRcSlots = MPROF_RC_CHAINS;
