@@ -37,7 +37,7 @@ namespace mpg {
 #ifndef MPROF_CHECKS
 #define MPROF_CHECKS 0
 #endif
-constexpr int kStageRowsMax = 256;  // largest rows-per-stage of any policy (checks only)
+constexpr int kStageRowsMax = 512;  // largest rows-per-stage of any policy (checks only)
 #if MPROF_CHECKS
 #define MPG_CHECK(cond) \
   do {                  \
@@ -588,7 +588,9 @@ struct Geo {
 // operands for stage st+1, so one copy of the K-wide window is resident (not two). Thresholds
 // (4 B per column) are re-read for the whole live window every stage (fresh minima from other
 // CTAs) and double-buffered with the row operands.
-template <class P, int D, int T, int S>
+// ROWA = false (the constant-row kernel, whose row operands are kernel parameters) drops the row
+// operand buffers.
+template <class P, int D, int T, int S, bool ROWA = true>
 struct SweepSmem {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
@@ -606,7 +608,7 @@ struct SweepSmem {
   static constexpr bool ZQ = P::kCovFilter && !P::kColScale && !EQ;
   static constexpr bool TW = !(ZQ || EQ);     // filters on threshold words (colBM2 / rowBM)
   int colBM2[TW ? NCB : 1];                    // max of colT over columns [cD, cD + 2D)
-  V2 rowA[2][S];                               // A[i0 + x]
+  V2 rowA[ROWA ? 2 : 1][ROWA ? S : 1];         // A[i0 + x]
   VB rowB[2][HASB ? S : 2];                    // B[i0 + 1 + x]
   int rowT[2][S];                              // hi32(best[i0 + 1 + x].v), exact
   int rowBM[TW ? S / D : 1];                   // max of rowT over aligned blocks of D
@@ -1289,8 +1291,8 @@ __device__ __forceinline__ float mu_up(float v) {
 }
 
 // Block maxima of the freshly loaded thresholds (after the stage's cp.async completed).
-template <class P, int D, int T, int S>
-__device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b, int X0) {
+template <class P, int D, int T, int S, bool ROWA = true>
+__device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S, ROWA>& sm, int b, int X0) {
   using G = Geo<D, T, S>;
   using SM = SweepSmem<P, D, T, S>;
   using VB = typename P::VB;
@@ -1451,7 +1453,7 @@ __device__ __forceinline__ void stage_block_max(SweepSmem<P, D, T, S>& sm, int b
 // its row operands and thresholds, the thresholds of its whole live column window, and the
 // column operands that enter the ring with it (all NCOL for stage 0, S afterwards).
 template <class P, int D, int T, int S, bool ROWA = true>
-__device__ __forceinline__ void load_stage(SweepSmem<P, D, T, S>& sm, const SweepParams& prm,
+__device__ __forceinline__ void load_stage(SweepSmem<P, D, T, S, ROWA>& sm, const SweepParams& prm,
                                            int st, int ra, int kb) {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;

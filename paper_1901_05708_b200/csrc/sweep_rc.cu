@@ -55,7 +55,7 @@ template <int D, int T, int S>
 constexpr int rc_stash_doubles() { return S / (kRcSuper * D) * D * T; }
 template <class P, int D, int T, int S>
 struct RcSmem {
-  SweepSmem<P, D, T, S> base;
+  SweepSmem<P, D, T, S, false> base;
   double stash[MPROF_RC_STASH_GLOBAL ? 1 : rc_stash_doubles<D, T, S>()];  // [super-group][d][thread]
 };
 
@@ -105,7 +105,7 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
                                              double* gstash) {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
-  using SMT = SweepSmem<P, D, T, S>;
+  using SMT = SweepSmem<P, D, T, S, false>;
   SMT& sm = rsm.base;
   constexpr bool EQ = SMT::EQ;
   static_assert(SMT::ZQ || SMT::EQ, "constant-row sweep: covariance-only filters");
@@ -238,7 +238,7 @@ template <class P, int D, int T, int S, int MINB>
 __global__ void __launch_bounds__(T, MINB)
     sweep_kernel_rc(const SweepParams prm, const __grid_constant__ RcParams rc) {
   using G = Geo<D, T, S>;
-  using SM = SweepSmem<P, D, T, S>;
+  using SM = SweepSmem<P, D, T, S, false>;
   using V = typename P::V;
   using VB = typename P::VB;
   static_assert(kRcW % S == 0, "a window is whole stages");
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(T, MINB)
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  stage_block_max<P, D, T, S>(sm, 0, 0);
+  stage_block_max<P, D, T, S, false>(sm, 0, 0);
   if (nst > 1) load_stage<P, D, T, S, false>(sm, prm, 1, ra, kb);
   cp_async_commit();
   __syncthreads();
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(T, MINB)
     if (st + 1 == nst) break;
     cp_async_wait<0>();
     __syncthreads();
-    stage_block_max<P, D, T, S>(sm, (st + 1) & 1, s0 + S);
+    stage_block_max<P, D, T, S, false>(sm, (st + 1) & 1, s0 + S);
     if (st + 2 < nst) load_stage<P, D, T, S, false>(sm, prm, st + 2, ra, kb);
     cp_async_commit();
     __syncthreads();
