@@ -96,6 +96,7 @@ struct Knobs {
   bool zn_no_near = false;      // MPROF_ZN_NO_NEAR: no column-scaled near-diagonal block
   bool stats = false;           // MPROF_STATS: count replays / offers (stderr)
   int aamp_cov = -1;            // MPROF_AAMP_COV=0|1: force the AAMP form (-1: by window spread)
+  bool no_graph = false;        // MPROF_NO_GRAPH: planned sweeps launch their window chain directly
 };
 const Knobs& knobs() {
   static const Knobs k = [] {
@@ -107,6 +108,7 @@ const Knobs& knobs() {
     r.zn_no_near = getenv("MPROF_ZN_NO_NEAR") != nullptr;
     r.stats = getenv("MPROF_STATS") != nullptr;
     if (const char* e = getenv("MPROF_AAMP_COV")) r.aamp_cov = atoi(e) ? 1 : 0;
+    r.no_graph = getenv("MPROF_NO_GRAPH") != nullptr;
     return r;
   }();
   return k;
@@ -927,6 +929,7 @@ struct mprof_plan {
   std::vector<mpg::RcBand> bands;  // constant-row part of the tile table
   int rc_policy = -1;
   double2* host_pairs = nullptr;   // owned pinned mirror of the operand pairs (constant-row sweep)
+  mpg::RcGraph rc_graph;           // the captured window chain
   bool aamp_cov = false, zn_colscale = false, wide = false, dense = false;
   unsigned long long probe_replays = 0;
   double probe_cells = 0.0;
@@ -1560,7 +1563,7 @@ int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams&
                        long long ntiles, long long n_near, long long n_legacy,
                        const std::vector<mpg::RcBand>& bands, int rc_policy,
                        const double2* host_pairs, int k1, bool first_diag, uint32_t* launches,
-                       float* ms, uint32_t* rc_launches) {
+                       float* ms, uint32_t* rc_launches, mpg::RcGraph* rc_graph = nullptr) {
   int32_t st = MPROF_OK;
   if (n_legacy < ntiles && !host_pairs) {  // before the timed region: the mirror needs a sync
     if (rc_policy < 0 || bands.empty()) return fail(MPROF_E_CUDA, "internal: row bands without a kernel");
@@ -1596,7 +1599,8 @@ int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams&
   if (n_legacy < ntiles) {
     if (rc_policy < 0 || bands.empty()) return fail(MPROF_E_CUDA, "internal: row bands without a kernel");
     uint32_t nl = 0;
-    const cudaError_t e = mpg::rc_sweep(rc_policy, prm, bands, c->rc, c->stream, host_pairs, &nl);
+    const cudaError_t e = mpg::rc_sweep(rc_policy, prm, bands, c->rc, c->stream, host_pairs, &nl,
+                                        rc_graph);
     if (e != cudaSuccess) return cuda_fail(e, "constant-row sweep");
     *launches += nl;
     if (rc_launches) *rc_launches += nl;
@@ -2852,6 +2856,7 @@ void mprof_plan_destroy(mprof_plan* P) {
   cudaFree(P->ws);
   cudaFree(P->tiles);
   if (P->host_pairs) cudaFreeHost(P->host_pairs);
+  mpg::rc_graph_release(P->rc_graph);
   delete P;
 }
 
@@ -2967,7 +2972,7 @@ int32_t mprof_plan_sweep(mprof_plan* P, double* d_cmp, int64_t* d_idx, mprof_run
     prm.R = (int)std::min<long long>(P->R, INT_MAX);
     int32_t st = dispatch_sweep(c, cfg, prm, P->ntiles, P->n_near, P->n_legacy, P->bands,
                                 P->rc_policy, P->host_pairs, (int)cfg->exclusion, true, &launches,
-                                &so.ms, &so.rc_launches);
+                                &so.ms, &so.rc_launches, knobs().no_graph ? nullptr : &P->rc_graph);
     if (st != MPROF_OK) return st;
     if (zn) {
       st = flat_fix(c, w.B, L, (int)P->k_lo, (int)P->k_hi, w, w.best, &launches);

@@ -32,7 +32,7 @@ static_assert(sizeof(SweepParams) + sizeof(RcParams) <= 32764, "kernel parameter
 // Rows per shared-memory stage of the constant-row kernels (their own choice: the window length is
 // a multiple of it, and the per-series rows-per-tile plan keeps using the legacy kernel's).
 #ifndef MPROF_RC_STAGE
-#define MPROF_RC_STAGE 256
+#define MPROF_RC_STAGE 384
 #endif
 template <class P>
 constexpr int rc_stage_rows_of() {
@@ -449,12 +449,76 @@ int rc_blocks_per_sm(int policy) {
   });
 }
 
+namespace {
+
+// Enqueues the window chain: fork from `main`, the bands' window launches round-robin over the
+// chain streams, join back into `main`.
+template <class P>
+cudaError_t rc_issue(const SweepParams& prm, const std::vector<RcBand>& bands, RcRes& res,
+                     cudaStream_t main, const double2* host_pairs, size_t per_tile,
+                     uint32_t* launches) {
+  auto kern = rc_kernel<P>();
+  const size_t smem = rc_smem<P>();
+  cudaError_t e2;
+  if ((e2 = cudaEventRecord(res.fork, main)) != cudaSuccess) return e2;
+  for (int s = 0; s < kRcSlots; ++s)
+    if ((e2 = cudaStreamWaitEvent(res.st[s], res.fork, 0)) != cudaSuccess) return e2;
+  // band i runs on chain i % kRcSlots; the chains are issued round-robin, one window launch at
+  // a time, so the streams advance together
+  size_t next_band[kRcSlots];
+  int next_w[kRcSlots];
+  for (int s = 0; s < kRcSlots; ++s) {
+    next_band[s] = (size_t)s;
+    next_w[s] = 0;
+  }
+  RcParams rc;
+  rc.zero = 0;
+  for (bool any = true; any;) {
+    any = false;
+    for (int s = 0; s < kRcSlots; ++s) {
+      while (next_band[s] < bands.size() && next_w[s] >= (int)bands[next_band[s]].count.size()) {
+        next_band[s] += kRcSlots;
+        next_w[s] = 0;
+      }
+      if (next_band[s] >= bands.size()) continue;
+      any = true;
+      const RcBand& bd = bands[next_band[s]];
+      const int w = next_w[s]++;
+      const int nt = bd.count[w];
+      if (nt <= 0) continue;
+      const long long r0 = (long long)bd.ra + (long long)w * kRcW;
+      const long long rows = std::min<long long>(kRcW, (long long)prm.L - 1 - r0);
+      if (rows > 0) std::memcpy(rc.rows, host_pairs + r0, (size_t)rows * sizeof(double2));
+      SweepParams q = prm;
+      q.tiles = prm.tiles + bd.off;
+      rc.w = w;
+      rc.acc = res.acc + (size_t)s * res.acc_tiles * per_tile;
+      kern<<<(unsigned)nt, kT, smem, res.st[s]>>>(q, rc);
+      if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+      ++*launches;
+    }
+  }
+  for (int s = 0; s < kRcSlots; ++s) {
+    if ((e2 = cudaEventRecord(res.join[s], res.st[s])) != cudaSuccess) return e2;
+    if ((e2 = cudaStreamWaitEvent(main, res.join[s], 0)) != cudaSuccess) return e2;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
 const double2* rc_pairs(int policy, const SweepParams& prm) {
   return (policy == kRcEuclidCov || policy == kRcWideEuclidCov) ? prm.A2 : prm.A;
 }
 
+void rc_graph_release(RcGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g = RcGraph{};
+}
+
 cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBand>& bands,
-                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches) {
+                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches,
+                     RcGraph* graph) {
   if (bands.empty()) return cudaSuccess;
   size_t most = 0;
   for (const RcBand& bd : bands)
@@ -464,54 +528,38 @@ cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBan
     constexpr size_t per_tile = (size_t)kD * kT + (MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<kD, kT, rc_stage_rows_of<P>()>() : 0);
     cudaError_t e = ensure_res(res, most, per_tile);
     if (e != cudaSuccess) return e;
-    auto kern = rc_kernel<P>();
-    const size_t smem = rc_smem<P>();
-    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e2 != cudaSuccess) return e2;
-    if ((e2 = cudaEventRecord(res.fork, main)) != cudaSuccess) return e2;
-    for (int s = 0; s < kRcSlots; ++s)
-      if ((e2 = cudaStreamWaitEvent(res.st[s], res.fork, 0)) != cudaSuccess) return e2;
-    // band i runs on chain i % kRcSlots; the chains are issued round-robin, one window launch at
-    // a time, so the streams advance together
-    size_t next_band[kRcSlots];
-    int next_w[kRcSlots];
-    for (int s = 0; s < kRcSlots; ++s) {
-      next_band[s] = (size_t)s;
-      next_w[s] = 0;
-    }
-    RcParams rc;
-    rc.zero = 0;
-    for (bool any = true; any;) {
-      any = false;
-      for (int s = 0; s < kRcSlots; ++s) {
-        while (next_band[s] < bands.size() &&
-               next_w[s] >= (int)bands[next_band[s]].count.size()) {
-          next_band[s] += kRcSlots;
-          next_w[s] = 0;
+    e = cudaFuncSetAttribute(rc_kernel<P>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rc_smem<P>());
+    if (e != cudaSuccess) return e;
+    if (graph && !prm.stats) {
+      // a graph is valid for the buffers its launches were captured with
+      if (graph->exec && (graph->acc != res.acc || graph->tiles != prm.tiles || graph->best != prm.best))
+        rc_graph_release(*graph);
+      if (!graph->exec) {
+        cudaGraph_t g = nullptr;
+        uint32_t n = 0;
+        if (cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+          const cudaError_t ei = rc_issue<P>(prm, bands, res, main, host_pairs, per_tile, &n);
+          const cudaError_t ec = cudaStreamEndCapture(main, &g);
+          if (ei == cudaSuccess && ec == cudaSuccess && g &&
+              cudaGraphInstantiate(&graph->exec, g, 0) == cudaSuccess) {
+            graph->acc = res.acc;
+            graph->tiles = prm.tiles;
+            graph->best = prm.best;
+            graph->launches = n;
+          } else {
+            graph->exec = nullptr;
+          }
+          if (g) cudaGraphDestroy(g);
         }
-        if (next_band[s] >= bands.size()) continue;
-        any = true;
-        const RcBand& bd = bands[next_band[s]];
-        const int w = next_w[s]++;
-        const int nt = bd.count[w];
-        if (nt <= 0) continue;
-        const long long r0 = (long long)bd.ra + (long long)w * kRcW;
-        const long long rows = std::min<long long>(kRcW, (long long)prm.L - 1 - r0);
-        if (rows > 0) std::memcpy(rc.rows, host_pairs + r0, (size_t)rows * sizeof(double2));
-        SweepParams q = prm;
-        q.tiles = prm.tiles + bd.off;
-        rc.w = w;
-        rc.acc = res.acc + (size_t)s * res.acc_tiles * per_tile;
-        kern<<<(unsigned)nt, kT, smem, res.st[s]>>>(q, rc);
-        if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
-        ++*launches;
+        cudaGetLastError();  // a stream that cannot be captured: direct launches below
+      }
+      if (graph->exec) {
+        if ((e = cudaGraphLaunch(graph->exec, main)) != cudaSuccess) return e;
+        *launches += graph->launches;
+        return cudaSuccess;
       }
     }
-    for (int s = 0; s < kRcSlots; ++s) {
-      if ((e2 = cudaEventRecord(res.join[s], res.st[s])) != cudaSuccess) return e2;
-      if ((e2 = cudaStreamWaitEvent(main, res.join[s], 0)) != cudaSuccess) return e2;
-    }
-    return cudaSuccess;
+    return rc_issue<P>(prm, bands, res, main, host_pairs, per_tile, launches);
   });
 }
 

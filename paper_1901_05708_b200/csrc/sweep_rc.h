@@ -31,12 +31,13 @@
 namespace mpg {
 
 // Rows per window (operand pairs of 16 bytes in the kernel parameter space, which holds 32 764
-// bytes in all; 1792 = 7 stages of 256 rows) and concurrent band chains (streams). Measured on C4
+// bytes in all; 1920 = 5 stages of 384 rows) and concurrent band chains (streams). Measured on C4
 // (sweep ms AAMP / ACAMP): 1920-row windows of 128-row stages, 8 chains 96.2 / 97.2, 16 chains
 // 95.0 / 96.3; 1792-row windows of 256-row stages (stash in global memory, 3 CTAs/SM), 8 chains
-// 91.7 / 92.4, 16 chains 90.0 / 91.5.
+// 91.7 / 92.4, 16 chains 90.0 / 91.5; 1920-row windows of 384-row stages (the longest stage that
+// keeps 3 CTAs/SM: 72 KB of shared memory without row-operand buffers), 16 chains 87.8 / 88.6.
 #ifndef MPROF_RC_W
-#define MPROF_RC_W 1792
+#define MPROF_RC_W 1920
 #endif
 #ifndef MPROF_RC_CHAINS
 #define MPROF_RC_CHAINS 16
@@ -67,6 +68,18 @@ struct RcRes {
   size_t acc_per_tile = 0;   // doubles per tile: the carry (K) and, optionally, the replay stash
 };
 
+// A captured window chain (planned sweeps): the ~600 launches of a sweep, each with 30 KB of
+// parameters, cost the host ~20 us apiece, which binds a GPU that sweeps only 1/8 of the
+// diagonals; a plan captures its chain once in a CUDA graph and replays it with one launch.
+struct RcGraph {
+  cudaGraphExec_t exec = nullptr;
+  const double* acc = nullptr;   // the carry buffer the graph's launches point into
+  const int4* tiles = nullptr;   // and their tile table
+  BestEntry* best = nullptr;
+  uint32_t launches = 0;
+};
+void rc_graph_release(RcGraph& g);
+
 // Rows per shared-memory stage of the policy's constant-row kernel.
 int rc_stage_rows(int policy);
 
@@ -77,8 +90,11 @@ int rc_blocks_per_sm(int policy);
 // kernel of `policy`: window launches chained per band on the context's chain streams, forked
 // from and joined to `main`. host_pairs = host copy of the policy's operand pairs (prm.A, or
 // prm.A2 for the covariance-form AAMP), L - 1 entries. Adds the kernel launches to *launches.
+// graph != nullptr: replay (or first capture) the chain as a CUDA graph; falls back to direct
+// launches when the stream cannot be captured.
 cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBand>& bands,
-                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches);
+                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches,
+                     RcGraph* graph = nullptr);
 
 // Device pointer of the policy's operand pairs in prm (what host_pairs must mirror).
 const double2* rc_pairs(int policy, const SweepParams& prm);
