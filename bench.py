@@ -74,6 +74,10 @@ def cells(n, m):
     return (n - m) * (n - m + 1) // 2
 
 
+def workload_name(engines, n, m):
+    return f"C4 {'+'.join(engines)}: n={n}, m={m}, exclusion 1, FP64"
+
+
 # ------------------------------------------------------------------------------------------------
 # clocks sampler (nvidia-smi DURING the timed region)
 
@@ -201,9 +205,14 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": DATA,
-        "config": {"workload": f"C4 {'+'.join(engines)}: bounded CPU sample of the n=2^20 series "
-                               f"(first {sample.size} samples), m={args.m}, exclusion 1, FP64",
-                   "n": int(sample.size), "m": args.m, "engines": engines},
+        # the same workload as the GPU arm; each timed step is a bounded sample of it (the first
+        # 2^17 samples of the same series, same m; profiles/r02_cpu_reference_c4.json holds a one-off
+        # full-size run of the same library on this pool's host cores)
+        "config": {"workload": workload_name(engines, args.n, args.m), "n": args.n, "m": args.m,
+                   "engines": engines,
+                   "sample": f"each step sweeps the first {sample.size} samples of the series "
+                             f"({step_cells:.3e} cells per step)",
+                   "parallelism": f"reference C++ library, {threads} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"first {sample.size} samples of the C4 series per engine per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -389,12 +398,12 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
-            "config": {"workload": f"C4 {'+'.join(engines)}: n={n}, m={m}, exclusion 1, FP64, "
-                                   f"{'(ranks sharing cuda:0, test mode) ' if share else ''}"
-                                   f"{('equal-area diagonal bands + fused peer-memory merge/finalize' if peers else 'equal-area diagonal bands + ncclMin merge + sharded finalize') if world > 1 else 'single GPU'}",
+            "config": {"workload": workload_name(engines, n, m),
                        "n": n, "m": m, "engines": engines, "cells_per_step": total_cells,
                        "l2": "flushed every step (256 MiB memset inside the timed region)",
-                       "parallelism": f"diagonal-band dp{world}"},
+                       "parallelism": f"diagonal-band dp{world}: "
+                                      f"{'(ranks sharing cuda:0, test mode) ' if share else ''}"
+                                      f"{('equal-area diagonal bands + fused peer-memory merge/finalize' if peers else 'equal-area diagonal bands + ncclMin merge + sharded finalize') if world > 1 else 'single GPU'}"},
             "roofline": roofline, "gpu_launches": launches[0], "clocks": clk}
 
     # the other BASELINE.json configurations (1 GPU): sweep-kernel times of each engine, so the

@@ -32,5 +32,5 @@ def test_bench_two_ranks_on_one_gpu():
     assert len(lines) == 1, r.stdout  # rank 0 alone prints
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["ms_per_step"] > 0
-    assert "fused peer-memory merge" in d["config"]["workload"]
+    assert "fused peer-memory merge" in d["config"]["parallelism"]
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0

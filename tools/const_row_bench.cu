@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps)
           const float th = fminf(__fmul_rd(rq.x, cq.y), __fmul_rd(cq.x, rq.y));
           const int theta = th > 0.f ? __double2hiint((double)th) : INT_MIN;
           int hb = INT_MIN;
+          unsigned long long hp64 = 0x8000000080000000ull;
 #pragma unroll
           for (int u = 0; u < D; ++u) {
             const double2 rr = SRC == 0 ? row[s + u] : crow[s + u];
@@ -59,9 +60,19 @@ __global__ void __launch_bounds__(T, 4) k(int* out, const double2* in, int reps)
               acc[d] = fma(rr.y, cc.x, fma(rr.x, cc.y, acc[d]));
               if (KEYS == 1 || (KEYS == 2 && (u == 3 || u == 7)) || (KEYS == 3 && u == 7))
                 hb = max(hb, __double2hiint(acc[d]));
+              if (KEYS == 4) {  // running maximum kept in the LOW word of a 64-bit register pair
+                int lo = (int)(unsigned)hp64;
+                lo = max(lo, __double2hiint(acc[d]));
+                hp64 = (hp64 & 0xffffffff00000000ull) | (unsigned)lo;
+                if (d == D - 1) asm volatile("" : "+l"(hp64));
+              }
+              if (KEYS == 5 && (d & 1)) {  // chain of 3-input maxima: m = max3(m, h[d-1], h[d])
+                hb = max(hb, max(__double2hiint(acc[d - 1]), __double2hiint(acc[d])));
+              }
             }
             c[u] = cp[g * (D + 1) + u];
           }
+          if (KEYS == 4) hb = (int)(unsigned)hp64;
           hit |= hb >= theta;
         }
         if (BR == 1) { if (hit) out[1] = s0; }
@@ -99,11 +110,13 @@ int main() {
   cudaMalloc(&out, 8); cudaMalloc(&in, 4096 * 16); cudaMemset(in, 0, 4096 * 16);
   double2 h[NS]; for (int i = 0; i < NS; ++i) h[i] = make_double2(1e-3 * i, 2e-3 * i);
   cudaMemcpyToSymbol(crow, h, sizeof(h));
-  for (int dyn : {0, 20 << 10, 40 << 10}) {
+  for (int dyn : {0}) {
     run<0, 1, 1>("smem keys branch/group", out, in, dyn);
     run<0, 1, 0>("smem keys deferred", out, in, dyn);
     run<1, 1, 1>("const keys branch/group", out, in, dyn);
     run<1, 1, 0>("const keys deferred", out, in, dyn);
+    run<1, 4, 0>("const keys lo-word chain", out, in, dyn);
+    run<1, 5, 0>("const keys max3 chain", out, in, dyn);
     run<1, 2, 0>("const keys@3,7 deferred", out, in, dyn);
     run<1, 3, 0>("const keys@7 deferred", out, in, dyn);
     run<0, 2, 0>("smem keys@3,7 deferred", out, in, dyn);

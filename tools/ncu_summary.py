@@ -86,11 +86,10 @@ def full(reps, tag: str):
     traffic = {}
     for name, d in summary.items():
         try:
-            rd = float(d["dram__bytes_read.sum"].split()[0])
-            wr = float(d["dram__bytes_write.sum"].split()[0])
-            unit = d["dram__bytes_read.sum"].split()[1]
-            mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            traffic[name] = (rd + wr) * mult
+            def nbytes(text):  # "31.5 Mbyte" -> bytes (each metric carries its own unit)
+                val, unit = text.split()[:2]
+                return float(val) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            traffic[name] = nbytes(d["dram__bytes_read.sum"]) + nbytes(d["dram__bytes_write.sum"])
         except (KeyError, ValueError, IndexError):
             pass
     js = {"tag": tag, "kernels": summary, "dram_bytes_per_launch_by_kernel": traffic,
