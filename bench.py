@@ -388,6 +388,9 @@ def main():
                 "peak_source": "measured live: mprof_fp64_peak (independent DFMA chains, 148 SMs, CUDA events)",
                 "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
                 "algorithmic_bytes_per_launch": 8 * n + 16 * L,
+                # the constant-row design's own HBM traffic: the accumulators of every live diagonal
+                # are stored and reloaded between two window launches (16 B per diagonal per boundary)
+                "window_carry_bytes_per_sweep_estimate": 16 * 1024 * (L // 1024) * nwin // 2 if nwin > 1 else 0,
                 "note": ("FP64-pipe bound (T and P/I are L2-resident: ~1e-4 B/cell); neither HBM nor "
                          "tensor cores. achieved/frac count SURVEY.md 8(d) algorithmic flops per cell "
                          "(AAMP 6, ACAMP 8); the kernel issues fewer FP64 instructions per cell "

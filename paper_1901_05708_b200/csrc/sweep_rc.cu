@@ -21,6 +21,8 @@ struct RcParams {
   int w;         // window index within the band's tiles
   int zero;      // 0, opaque to the compiler (run_stage_rc's per-thread replay offsets)
   double* acc;   // accumulator carry of the launch's chain: [tile][K]
+  double* stash;          // replay stash pool: [SM][kRcSmSlots][super-group][d][thread]
+  unsigned* stash_bits;   // per SM bitmap of taken stash slots
   double2 rows[kRcW];  // operand pairs of the window's row transitions
 };
 static_assert(sizeof(SweepParams) + sizeof(RcParams) <= 32764, "kernel parameter space");
@@ -45,9 +47,12 @@ constexpr int rc_stage_rows_of() {
 #define MPROF_RC_SUPER 8
 #endif
 constexpr int kRcSuper = MPROF_RC_SUPER;  // blocks per stash
-// MPROF_RC_STASH_GLOBAL = 1 (default) keeps the stash in global memory instead (per resident CTA
-// S / 64 x 8 KB that stay in L2: 64 bytes stored per thread per 512 cells), which frees 32 KB of
-// shared memory per CTA at 256-row stages: 3 CTAs per SM instead of 2 (C4 AAMP 94.6 -> 90.0 ms).
+// MPROF_RC_STASH_GLOBAL = 1 (default) keeps the stash in global memory instead (64 bytes stored
+// per thread per 512 cells), which frees 32 KB of shared memory per CTA at 256-row stages: 3 CTAs
+// per SM instead of 2 (C4 AAMP 94.6 -> 90.0 ms). A CTA takes its S / 64 x 8 KB from a pool with
+// kRcSmSlots slots per SM (claimed in the SM's bitmap at the start, released at the end), so the
+// stash is 148 x 8 x 48 KB = 57 MB that live in L2; a stash per tile of every chain (0.8 GB at C4)
+// was written back to HBM as the chains evicted each other: 23 MB per window launch.
 #ifndef MPROF_RC_STASH_GLOBAL
 #define MPROF_RC_STASH_GLOBAL 1
 #endif
@@ -263,10 +268,7 @@ __global__ void __launch_bounds__(T, MINB)
     if (threadIdx.x == 0) g_cell_ctx = CellCtx{prm.S, prm.mu, static_cast<double>(m)};
     __syncthreads();
   }
-  // per tile of the launch: [carry K | stash] doubles
-  constexpr int kPerTile = G::K + (MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<D, T, S>() : 0);
-  double* carry = rc.acc + (static_cast<size_t>(blockIdx.x) * kPerTile + threadIdx.x * D);
-  double* gstash = rc.acc + (static_cast<size_t>(blockIdx.x) * kPerTile + G::K);
+  double* carry = rc.acc + (static_cast<size_t>(blockIdx.x) * G::K + threadIdx.x * D);
   V acc[D];
   if (rc.w == 0) {
     // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d), as sweep_kernel ----
@@ -342,6 +344,27 @@ __global__ void __launch_bounds__(T, MINB)
     }
   }
 
+  // ---- the CTA's replay stash: a slot of the per-SM pool (claimed in the SM's bitmap, released
+  // at the end; the pool has more slots per SM than CTAs can be resident) ----
+  double* gstash = nullptr;
+  if constexpr (MPROF_RC_STASH_GLOBAL) {
+    __shared__ int s_slot;
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      int got = -1;
+      while (got < 0) {
+        for (int bsl = 0; bsl < kRcSmSlots && got < 0; ++bsl) {
+          const unsigned bit = 1u << bsl;
+          if (!(atomicOr(&rc.stash_bits[smid], bit) & bit)) got = bsl;
+        }
+      }
+      s_slot = static_cast<int>(smid) * kRcSmSlots + got;
+    }
+    __syncthreads();
+    gstash = rc.stash + static_cast<size_t>(s_slot) * rc_stash_doubles<D, T, S>();
+  }
+
   // ---- stage pipeline over the window's row transitions (sweep_kernel's, rows from rc.rows) --
   const typename P::V2* A = pairs_of<P>(prm);
   const int nst = (steps + S - 1) / S;
@@ -373,6 +396,15 @@ __global__ void __launch_bounds__(T, MINB)
     if (st + 2 < nst) load_stage<P, D, T, S, false>(sm, prm, st + 2, ra, kb);
     cp_async_commit();
     __syncthreads();
+  }
+  if constexpr (MPROF_RC_STASH_GLOBAL) {
+    __syncthreads();  // every thread is done with the stash
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int bsl = (static_cast<int>((gstash - rc.stash) / rc_stash_doubles<D, T, S>())) % kRcSmSlots;
+      atomicAnd(&rc.stash_bits[smid], ~(1u << bsl));
+    }
   }
   // more transitions of this tile follow in the next window: carry the accumulators
   if (left > kRcW) {
@@ -410,7 +442,7 @@ auto with_rc_policy(int policy, F&& f) {
 #endif
 }
 
-cudaError_t ensure_res(RcRes& res, size_t tiles, size_t per_tile) {
+cudaError_t ensure_res(RcRes& res, size_t tiles, size_t per_tile, size_t stash_doubles) {
   cudaError_t e;
   if (!res.fork) {
     if ((e = cudaEventCreateWithFlags(&res.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -418,6 +450,20 @@ cudaError_t ensure_res(RcRes& res, size_t tiles, size_t per_tile) {
       if ((e = cudaStreamCreateWithFlags(&res.st[s], cudaStreamNonBlocking)) != cudaSuccess) return e;
       if ((e = cudaEventCreateWithFlags(&res.join[s], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
+  }
+  if (stash_doubles > 0 && (stash_doubles != res.stash_slot_doubles || !res.stash)) {
+    int dev = 0, sms = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if (res.stash) cudaFree(res.stash);
+    if (res.stash_bits) cudaFree(res.stash_bits);
+    res.stash = nullptr;
+    res.stash_bits = nullptr;
+    if ((e = cudaMalloc(&res.stash, sizeof(double) * stash_doubles * sms * kRcSmSlots)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&res.stash_bits, sizeof(unsigned) * sms)) != cudaSuccess) return e;
+    if ((e = cudaMemset(res.stash_bits, 0, sizeof(unsigned) * sms)) != cudaSuccess) return e;
+    res.stash_slot_doubles = stash_doubles;
+    res.stash_sms = sms;
   }
   if (tiles * per_tile > res.acc_tiles * res.acc_per_tile || per_tile != res.acc_per_tile) {
     if (res.acc) cudaFree(res.acc);
@@ -493,6 +539,8 @@ cudaError_t rc_issue(const SweepParams& prm, const std::vector<RcBand>& bands, R
       q.tiles = prm.tiles + bd.off;
       rc.w = w;
       rc.acc = res.acc + (size_t)s * res.acc_tiles * per_tile;
+      rc.stash = res.stash;
+      rc.stash_bits = res.stash_bits;
       kern<<<(unsigned)nt, kT, smem, res.st[s]>>>(q, rc);
       if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
       ++*launches;
@@ -525,14 +573,16 @@ cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBan
     if (!bd.count.empty()) most = std::max<size_t>(most, (size_t)bd.count[0]);
   if (most == 0) return cudaSuccess;
   return with_rc_policy(policy, [&]<class P>() -> cudaError_t {
-    constexpr size_t per_tile = (size_t)kD * kT + (MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<kD, kT, rc_stage_rows_of<P>()>() : 0);
-    cudaError_t e = ensure_res(res, most, per_tile);
+    constexpr size_t per_tile = (size_t)kD * kT;
+    constexpr size_t stash_doubles = MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<kD, kT, rc_stage_rows_of<P>()>() : 0;
+    cudaError_t e = ensure_res(res, most, per_tile, stash_doubles);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(rc_kernel<P>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rc_smem<P>());
     if (e != cudaSuccess) return e;
     if (graph && !prm.stats) {
       // a graph is valid for the buffers its launches were captured with
-      if (graph->exec && (graph->acc != res.acc || graph->tiles != prm.tiles || graph->best != prm.best))
+      if (graph->exec && (graph->acc != res.acc || graph->stash != res.stash ||
+                          graph->tiles != prm.tiles || graph->best != prm.best))
         rc_graph_release(*graph);
       if (!graph->exec) {
         cudaGraph_t g = nullptr;
@@ -543,6 +593,7 @@ cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBan
           if (ei == cudaSuccess && ec == cudaSuccess && g &&
               cudaGraphInstantiate(&graph->exec, g, 0) == cudaSuccess) {
             graph->acc = res.acc;
+            graph->stash = res.stash;
             graph->tiles = prm.tiles;
             graph->best = prm.best;
             graph->launches = n;
@@ -582,6 +633,11 @@ void rc_release(RcRes& res) {
   if (res.acc) cudaFree(res.acc);
   res.acc = nullptr;
   res.acc_tiles = 0;
+  if (res.stash) cudaFree(res.stash);
+  if (res.stash_bits) cudaFree(res.stash_bits);
+  res.stash = nullptr;
+  res.stash_bits = nullptr;
+  res.stash_slot_doubles = 0;
 }
 
 }  // namespace mpg

@@ -44,6 +44,7 @@ namespace mpg {
 #endif
 constexpr int kRcW = MPROF_RC_W;
 constexpr int kRcSlots = MPROF_RC_CHAINS;
+constexpr int kRcSmSlots = 8;   // stash slots per SM (>= resident CTAs per SM)
 static_assert(kRcW * 16 <= 30720, "the row window must fit the kernel parameter space");
 
 enum RcPolicy { kRcZnorm = 0, kRcWideZnorm = 1, kRcEuclidCov = 2, kRcWideEuclidCov = 3 };
@@ -65,7 +66,13 @@ struct RcRes {
   cudaEvent_t join[kRcSlots] = {};
   double* acc = nullptr;     // kRcSlots (chains) x acc_tiles x K doubles
   size_t acc_tiles = 0;
-  size_t acc_per_tile = 0;   // doubles per tile: the carry (K) and, optionally, the replay stash
+  size_t acc_per_tile = 0;   // doubles per tile: the carry (K)
+  // replay stash pool: one slot per resident CTA (kRcSmSlots per SM, claimed in a per-SM bitmap),
+  // so the stash stays a few tens of MB that live in L2 whatever the number of tiles
+  double* stash = nullptr;
+  unsigned* stash_bits = nullptr;   // per SM: bit b set = slot b taken
+  size_t stash_slot_doubles = 0;
+  int stash_sms = 0;
 };
 
 // A captured window chain (planned sweeps): the ~600 launches of a sweep, each with 30 KB of
@@ -74,6 +81,7 @@ struct RcRes {
 struct RcGraph {
   cudaGraphExec_t exec = nullptr;
   const double* acc = nullptr;   // the carry buffer the graph's launches point into
+  const double* stash = nullptr; // and the stash pool
   const int4* tiles = nullptr;   // and their tile table
   BestEntry* best = nullptr;
   uint32_t launches = 0;
