@@ -7,12 +7,14 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1901_05708_b200 as mp  # noqa: E402
 from paper_1901_05708_b200 import workloads as W  # noqa: E402
 
-args = [a for a in sys.argv[1:] if a != "norc"]
+args = [a for a in sys.argv[1:] if a not in ("norc", "rcall")]
 names = args or ["C4aamp", "C4acamp"]
 ctx = mp.Context(0)
 ctx.set_timing(True)
 if "norc" in sys.argv[1:]:
     ctx.set_row_const(False)  # the legacy single-launch tile kernel
+if "rcall" in sys.argv[1:]:
+    ctx.set_row_const(2)      # the constant-row kernel for every covariance-only form
 out = {}
 for name in names:
     c = W.CONFIGS[name]
