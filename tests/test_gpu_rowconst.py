@@ -65,3 +65,27 @@ def test_row_const_bands_merge_to_the_single_sweep(series):
     assert whole.info.row_windows > 0
     np.testing.assert_array_equal(whole.nn_index, parts.nn_index)
     np.testing.assert_array_equal(whole.distances.view(np.uint64), parts.distances.view(np.uint64))
+
+
+@pytest.mark.parametrize("family", ["aamp", "acamp"])
+def test_row_const_replay_heavy_series_bit_identical(family):
+    """A near-periodic series with a low noise floor (the C3 recipe): the covariance-only filters
+    pass and replay a large share of their blocks, so the constant-row kernel's deferred replays
+    (stash restart, fast-forward of the groups that did not pass, partial last stages) decide most
+    entries; they must reproduce the tile kernel's in-place replays bit for bit."""
+    t = W.c3(n=1 << 15)
+    kind = mp.DistanceKind.euclidean() if family == "aamp" else mp.DistanceKind.znormalized()
+    fn = mp.aamp if family == "aamp" else mp.acamp
+    out = []
+    for rc in (2, 0):
+        ctx = mp.Context(0)
+        ctx.set_form(mp.Form.Cov)
+        ctx.set_row_const(rc)
+        cfg = mp.ProfileConfig(256, kind)
+        cfg.exclusion = 64
+        out.append(fn(mp.make_time_series(t), cfg, ctx=ctx))
+        ctx.close()
+    a, b = out
+    assert a.info.row_windows > 0 and b.info.row_windows == 0
+    np.testing.assert_array_equal(a.nn_index, b.nn_index)
+    np.testing.assert_array_equal(a.distances.view(np.uint64), b.distances.view(np.uint64))
