@@ -151,10 +151,9 @@ int32_t mprof_ctx_set_progress(mprof_ctx* ctx, mprof_progress_fn fn, void* user)
 enum { MPROF_FORM_AUTO = 0, MPROF_FORM_COV = 1, MPROF_FORM_WIDE = 2, MPROF_FORM_ALT = 3,
        MPROF_FORM_DENSE = 4 };
 int32_t mprof_ctx_set_form(mprof_ctx* ctx, int32_t form);
-/* Constant-row sweep (1, the default): the FP64 covariance-only forms with long hit groups
- * (Wide<EuclidCov>, Wide<Znorm<0>>: series whose form probe saw almost no replays; 2: also
- * EuclidCov and Znorm<0>, whose replay-heavy series run faster on the tile kernel)
- * run as a sequence of row-window launches (1920 rows each) with the row operands passed as kernel
+/* Constant-row sweep (nonzero, the default): the FP64 covariance-only forms (EuclidCov, Znorm<0>
+ * and their Wide<> variants, i.e. the sweeps of >= 4e9 cells the form probe confirms) run as a
+ * sequence of row-window launches (1920 rows each) with the row operands passed as kernel
  * parameters, i.e. in the constant bank (uniform-register DFMA operands); 0 keeps the
  * single-launch tile kernel. Both paths do the same arithmetic per cell: identical P and I
  * (tests/test_gpu_rowconst.py). Anytime sweeps (a progress observer) use the tile kernel. */

@@ -386,8 +386,8 @@ class Context:
         _raise(lib().mprof_ctx_set_form(self.handle, int(form)))
 
     def set_row_const(self, on) -> None:
-        """Constant-row sweep (mprof_ctx_set_row_const): True / 1 (default) for the Wide<> forms,
-        2 for every covariance-only form, False / 0 off."""
+        """Constant-row sweep of the covariance-only forms (mprof_ctx_set_row_const): on by
+        default; False / 0 selects the single-launch tile kernel."""
         _raise(lib().mprof_ctx_set_row_const(self.handle, int(on)))
 
     def close(self) -> None:

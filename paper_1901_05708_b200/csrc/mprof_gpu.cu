@@ -868,7 +868,6 @@ struct mprof_ctx {
   // constant-row sweep (sweep_rc.h): streams, events, accumulator carry; on by default
   mpg::RcRes rc;
   bool rowconst = true;
-  bool rowconst_all = false;  // also for the non-Wide covariance-only forms (set_row_const 2)
   // pinned host copy of the operand pairs the window launches pass as kernel parameters, valid
   // for operand generation rc_host_gen of device array rc_host_src (prepare_operands bumps op_gen)
   double2* rc_host = nullptr;
@@ -1524,12 +1523,10 @@ int rc_policy_of(const mprof_ctx* c, const mprof_config* cfg, long long R) {
   // (anytime sweeps run many small chunks: the legacy kernel's single launch per chunk)
   if (!c->rowconst || cfg->exact || cfg->precision != MPROF_FP64 || c->dense || c->progress) return -1;
   if (R <= 0) return -1;
-  // Only the Wide<> forms by default, i.e. series whose probe sample saw (almost) no replays: the
-  // constant-row kernel defers its replays to the end of a stage and restarts them from the
-  // super-group's stash, which costs more per replay than the tile kernel's in-place replay
-  // (C5, Znorm<0> with ~1e8 replayed blocks: 2737 ms against the tile kernel's 2100 ms).
-  // mprof_ctx_set_row_const(ctx, 2) forces it for every covariance-only form (tests).
-  if (!c->wide && c->rowconst_all == false) return -1;
+  // Every covariance-only form: the replay-heavy ones (hit groups of 2, e.g. C5) stash their
+  // accumulators per hit group, so a deferred replay restarts at its own group (sweep_rc.cu):
+  // C5 2100 -> 1805 ms, random walk n = 2^20, m = 512 ACAMP 131.7 -> 114.4 ms; small sweeps
+  // (n = 2^17, m = 512: 3.29 vs 3.34 ms) are neutral.
   if (cfg->family == MPROF_ZNORMALIZED)
     return c->zn_colscale ? -1 : (c->wide ? mpg::kRcWideZnorm : mpg::kRcZnorm);
   const bool l2 = cfg->family == MPROF_EUCLIDEAN || (cfg->family == MPROF_PNORM && cfg->p == 2.0);
@@ -3002,7 +2999,6 @@ int32_t mprof_ctx_set_row_const(mprof_ctx* in, int32_t enabled) {
   int32_t st = resolve_ctx(in, &c);
   if (st != MPROF_OK) return st;
   c->rowconst = enabled != 0;
-  c->rowconst_all = enabled == 2;
   return MPROF_OK;
 }
 

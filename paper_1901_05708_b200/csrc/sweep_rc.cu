@@ -46,7 +46,18 @@ constexpr int rc_stage_rows_of() {
 #ifndef MPROF_RC_SUPER
 #define MPROF_RC_SUPER 8
 #endif
-constexpr int kRcSuper = MPROF_RC_SUPER;  // blocks per stash
+constexpr int kRcSuper = MPROF_RC_SUPER;  // blocks per stash (policies with long hit groups)
+// Blocks per stash of policy P: its hit group when that is shorter (MPROF_RC_SUPER_FINE = 1): a
+// passing group is then replayed straight from its own stash, without fast-forwarding through the
+// groups before it -- what the replay-heavy forms (hit groups of 2) need; 0 keeps kRcSuper.
+#ifndef MPROF_RC_SUPER_FINE
+#define MPROF_RC_SUPER_FINE 1
+#endif
+template <class P>
+constexpr int rc_super_of() {
+  constexpr int hg = hit_group_for<P>();
+  return (MPROF_RC_SUPER_FINE && hg < kRcSuper) ? hg : kRcSuper;
+}
 // MPROF_RC_STASH_GLOBAL = 1 (default) keeps the stash in global memory instead (64 bytes stored
 // per thread per 512 cells), which frees 32 KB of shared memory per CTA at 256-row stages: 3 CTAs
 // per SM instead of 2 (C4 AAMP 94.6 -> 90.0 ms). A CTA takes its S / 64 x 8 KB from a pool with
@@ -56,12 +67,12 @@ constexpr int kRcSuper = MPROF_RC_SUPER;  // blocks per stash
 #ifndef MPROF_RC_STASH_GLOBAL
 #define MPROF_RC_STASH_GLOBAL 1
 #endif
-template <int D, int T, int S>
-constexpr int rc_stash_doubles() { return S / (kRcSuper * D) * D * T; }
+template <class P, int D, int T, int S>
+constexpr int rc_stash_doubles() { return S / (rc_super_of<P>() * D) * D * T; }
 template <class P, int D, int T, int S>
 struct RcSmem {
   SweepSmem<P, D, T, S, false> base;
-  double stash[MPROF_RC_STASH_GLOBAL ? 1 : rc_stash_doubles<D, T, S>()];  // [super-group][d][thread]
+  double stash[MPROF_RC_STASH_GLOBAL ? 1 : rc_stash_doubles<P, D, T, S>()];  // [super-group][d][thread]
 };
 
 // The slide of one block without any cell test (bit-identical to the hot loop's and to
@@ -116,9 +127,10 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
   static_assert(SMT::ZQ || SMT::EQ, "constant-row sweep: covariance-only filters");
   static_assert(sizeof(typename P::V) == 8, "constant-row sweep: FP64");
   constexpr int HG = hit_group_for<P>();
-  static_assert(kRcSuper % HG == 0 && S % (kRcSuper * D) == 0, "super-groups are whole hit groups");
-  constexpr int GPS = kRcSuper / HG;         // hit groups per super-group
-  constexpr int NSG = S / (kRcSuper * D);    // super-groups per stage
+  constexpr int SUP = rc_super_of<P>();      // blocks per stash
+  static_assert(SUP % HG == 0 && S % (SUP * D) == 0, "super-groups are whole hit groups");
+  constexpr int GPS = SUP / HG;              // hit groups per super-group
+  constexpr int NSG = S / (SUP * D);         // super-groups per stage
   static_assert(NSG * GPS <= 32, "one hit bit per group");
   constexpr int RP = G::RING / D * (D + 1);  // padded ring length
   const int xb = threadIdx.x * D;
@@ -154,7 +166,7 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
   const int lim = GUARD ? cnt : S;  // full stages: a compile-time trip count
   int sg = 0;
 #pragma unroll 1
-  for (int s0 = 0; s0 < lim; s0 += kRcSuper * D, ++sg) {
+  for (int s0 = 0; s0 < lim; s0 += SUP * D, ++sg) {
 #pragma unroll
     for (int d = 0; d < D; ++d) stash[(sg * D + d) * T] = acc[d];
 #pragma unroll
@@ -193,13 +205,13 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
       }
       hmask |= (hit ? 1u : 0u) << (sg * GPS + gg);
     }
-    ci += kRcSuper * D;
+    ci += SUP * D;
     if constexpr (EQ) {
-      ect += kRcSuper;
-      ert += kRcSuper;
+      ect += SUP;
+      ert += SUP;
     } else {
-      zct += kRcSuper;
-      zrt += kRcSuper;
+      zct += SUP;
+      zrt += SUP;
     }
   }
   if (hmask == 0) return;
@@ -212,8 +224,8 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
   for (int g2 = 0; g2 < NSG; ++g2) {
     const unsigned bits = (hmask >> (g2 * GPS)) & ((1u << GPS) - 1u);
     if (bits == 0) {
-      sv += kRcSuper * D;
-      q1 += kRcSuper * (D + 1);
+      sv += SUP * D;
+      q1 += SUP * (D + 1);
       if (q1 >= RP) q1 -= RP;
       continue;
     }
@@ -221,7 +233,7 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
 #pragma unroll
     for (int d = 0; d < D; ++d) a0.a[d] = stash[(g2 * D + d) * T];
 #pragma unroll 1
-    for (int g = 0; g < kRcSuper; ++g) {
+    for (int g = 0; g < SUP; ++g) {
       if (GUARD && sv >= cnt) break;
       int q2 = q1 + (D + 1);
       if (q2 >= RP) q2 -= RP;
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(T, MINB)
       s_slot = static_cast<int>(smid) * kRcSmSlots + got;
     }
     __syncthreads();
-    gstash = rc.stash + static_cast<size_t>(s_slot) * rc_stash_doubles<D, T, S>();
+    gstash = rc.stash + static_cast<size_t>(s_slot) * rc_stash_doubles<P, D, T, S>();
   }
 
   // ---- stage pipeline over the window's row transitions (sweep_kernel's, rows from rc.rows) --
@@ -402,7 +414,7 @@ __global__ void __launch_bounds__(T, MINB)
     if (threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      const int bsl = (static_cast<int>((gstash - rc.stash) / rc_stash_doubles<D, T, S>())) % kRcSmSlots;
+      const int bsl = (static_cast<int>((gstash - rc.stash) / rc_stash_doubles<P, D, T, S>())) % kRcSmSlots;
       atomicAnd(&rc.stash_bits[smid], ~(1u << bsl));
     }
   }
@@ -574,7 +586,7 @@ cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBan
   if (most == 0) return cudaSuccess;
   return with_rc_policy(policy, [&]<class P>() -> cudaError_t {
     constexpr size_t per_tile = (size_t)kD * kT;
-    constexpr size_t stash_doubles = MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<kD, kT, rc_stage_rows_of<P>()>() : 0;
+    constexpr size_t stash_doubles = MPROF_RC_STASH_GLOBAL ? rc_stash_doubles<P, kD, kT, rc_stage_rows_of<P>()>() : 0;
     cudaError_t e = ensure_res(res, most, per_tile, stash_doubles);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(rc_kernel<P>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rc_smem<P>());

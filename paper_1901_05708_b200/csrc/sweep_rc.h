@@ -44,7 +44,7 @@ namespace mpg {
 #endif
 constexpr int kRcW = MPROF_RC_W;
 constexpr int kRcSlots = MPROF_RC_CHAINS;
-constexpr int kRcSmSlots = 8;   // stash slots per SM (>= resident CTAs per SM)
+constexpr int kRcSmSlots = 4;   // stash slots per SM (>= resident CTAs per SM: 3)
 static_assert(kRcW * 16 <= 30720, "the row window must fit the kernel parameter space");
 
 enum RcPolicy { kRcZnorm = 0, kRcWideZnorm = 1, kRcEuclidCov = 2, kRcWideEuclidCov = 3 };

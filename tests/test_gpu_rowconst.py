@@ -21,7 +21,7 @@ def series():
 def run(series, family, form, excl, row_const, k_lo=0, k_hi=0):
     ctx = mp.Context(0)
     ctx.set_form(form)
-    ctx.set_row_const(2 if row_const else 0)  # 2: also the non-Wide covariance-only forms
+    ctx.set_row_const(row_const)
     kind = mp.DistanceKind.euclidean() if family == "aamp" else mp.DistanceKind.znormalized()
     cfg = mp.ProfileConfig(M, kind)
     cfg.exclusion = excl
@@ -77,7 +77,7 @@ def test_row_const_replay_heavy_series_bit_identical(family):
     kind = mp.DistanceKind.euclidean() if family == "aamp" else mp.DistanceKind.znormalized()
     fn = mp.aamp if family == "aamp" else mp.acamp
     out = []
-    for rc in (2, 0):
+    for rc in (1, 0):
         ctx = mp.Context(0)
         ctx.set_form(mp.Form.Cov)
         ctx.set_row_const(rc)

@@ -14,6 +14,9 @@ python tools/time_c4.py C4acamp > /dev/null && ncu --set full --clock-control no
 python tools/time_c4.py C4aamp C4acamp C5 C2 C3p1 C3p3 C1 > gpurun_out/time_c4.json 2>&1
 # summarise on the box (two --set full reports exceed gpurun's 64 MiB copy-back limit)
 python tools/ncu_summary.py $TAG --launches gpurun_out/launches.csv --rep gpurun_out/aamp.ncu-rep --rep gpurun_out/acamp.ncu-rep > gpurun_out/summary.log 2>&1
+# DRAM traffic of the window launches from a single-pass run (tools/window_traffic.py says why)
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/win_traffic.csv --kernel-name-base demangled -k regex:sweep_kernel_rc -s 60 -c 300 python tools/time_c4.py C4aamp C4acamp > gpurun_out/win_traffic.log 2>&1
+python tools/window_traffic.py gpurun_out/win_traffic.csv $TAG >> gpurun_out/summary.log 2>&1
 cp profiles/${TAG}_* profiles/ncu_summary.json gpurun_out/
 rm -f gpurun_out/acamp.ncu-rep
 ls -la gpurun_out
