@@ -463,7 +463,9 @@ cudaError_t ensure_res(RcRes& res, size_t tiles, size_t per_tile, size_t stash_d
       if ((e = cudaEventCreateWithFlags(&res.join[s], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
   }
-  if (stash_doubles > 0 && (stash_doubles != res.stash_slot_doubles || !res.stash)) {
+  // grow-only: a pool sized for the largest slot serves every policy (each kernel strides the pool
+  // by its own slot size), so alternating policies on one context do not reallocate
+  if (stash_doubles > 0 && (stash_doubles > res.stash_slot_doubles || !res.stash)) {
     int dev = 0, sms = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;

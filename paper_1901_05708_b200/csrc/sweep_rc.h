@@ -11,7 +11,7 @@
 // (DFMA R, R, UR, R: two vector register reads). A tile (1024 diagonals x R rows, the legacy
 // kernel's CTA) becomes ceil(R / kRcW) consecutive window launches that carry their accumulators
 // through a global buffer; the tiles that start at the same row form a band whose windows are
-// chained on one stream, and the bands run concurrently on kRcChains streams (each launch has at
+// chained on one stream, and the bands run concurrently on kRcSlots streams (each launch has at
 // most L / 1024 CTAs: the chains fill each other's tails). Every cell keeps the arithmetic of the
 // legacy kernel (same seeds on the same row grid, same slide order), so the two paths give
 // bit-identical profiles (tests/test_gpu_rowconst.py).
