@@ -47,16 +47,18 @@ constexpr int rc_stage_rows_of() {
 #define MPROF_RC_SUPER 8
 #endif
 constexpr int kRcSuper = MPROF_RC_SUPER;  // blocks per stash (policies with long hit groups)
-// Blocks per stash of policy P: its hit group when that is shorter (MPROF_RC_SUPER_FINE = 1): a
-// passing group is then replayed straight from its own stash, without fast-forwarding through the
-// groups before it -- what the replay-heavy forms (hit groups of 2) need; 0 keeps kRcSuper.
+// Blocks per stash of policy P: MPROF_RC_SUPER_FINE blocks (at least its hit group) when its hit
+// group is shorter than kRcSuper: a passing group is then replayed from a stash at most
+// MPROF_RC_SUPER_FINE - hit group blocks before it instead of fast-forwarding through up to 7
+// blocks -- what the replay-heavy forms (hit groups of 2) need; 0 keeps kRcSuper.
 #ifndef MPROF_RC_SUPER_FINE
-#define MPROF_RC_SUPER_FINE 1
+#define MPROF_RC_SUPER_FINE 2
 #endif
 template <class P>
 constexpr int rc_super_of() {
   constexpr int hg = hit_group_for<P>();
-  return (MPROF_RC_SUPER_FINE && hg < kRcSuper) ? hg : kRcSuper;
+  if constexpr (MPROF_RC_SUPER_FINE == 0 || hg >= kRcSuper) return kRcSuper;
+  else return hg > MPROF_RC_SUPER_FINE ? hg : MPROF_RC_SUPER_FINE;
 }
 // MPROF_RC_STASH_GLOBAL = 1 (default) keeps the stash in global memory instead (64 bytes stored
 // per thread per 512 cells), which frees 32 KB of shared memory per CTA at 256-row stages: 3 CTAs
