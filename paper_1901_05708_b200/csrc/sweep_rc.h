@@ -36,11 +36,15 @@ namespace mpg {
 // 95.0 / 96.3; 1792-row windows of 256-row stages (stash in global memory, 3 CTAs/SM), 8 chains
 // 91.7 / 92.4, 16 chains 90.0 / 91.5; 1920-row windows of 384-row stages (the longest stage that
 // keeps 3 CTAs/SM: 72 KB of shared memory without row-operand buffers), 16 chains 87.8 / 88.6.
+// 32 chains (one per row band at C4) measure the same on one GPU (86.6 / 86.8) but matter when a
+// GPU sweeps 1/8 of the diagonals: its launches have ~100 CTAs, a chain's windows run one after
+// the other, and with 16 chains the 36 windows per chain (~300 us each) bound the band at
+// 12.7-14.3 ms; with 32 chains the slowest of 8 bands takes 12.0 / 11.6 ms (90 % / 94 % of 1/8).
 #ifndef MPROF_RC_W
 #define MPROF_RC_W 1920
 #endif
 #ifndef MPROF_RC_CHAINS
-#define MPROF_RC_CHAINS 16
+#define MPROF_RC_CHAINS 32
 #endif
 constexpr int kRcW = MPROF_RC_W;
 constexpr int kRcSlots = MPROF_RC_CHAINS;
