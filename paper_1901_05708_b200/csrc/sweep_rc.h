@@ -39,7 +39,7 @@ namespace mpg {
 // 32 chains (one per row band at C4) measure the same on one GPU (86.6 / 86.8) but matter when a
 // GPU sweeps 1/8 of the diagonals: its launches have ~100 CTAs, a chain's windows run one after
 // the other, and with 16 chains the 36 windows per chain (~300 us each) bound the band at
-// 12.7-14.3 ms; with 32 chains the slowest of 8 bands takes 12.0 / 11.6 ms (90 % / 94 % of 1/8).
+// 12.7-14.3 ms; with 32 chains the slowest of 8 bands takes 11.8 / 11.6 ms (92 % / 94 % of 1/8).
 #ifndef MPROF_RC_W
 #define MPROF_RC_W 1920
 #endif
