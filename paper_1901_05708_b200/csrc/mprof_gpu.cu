@@ -870,9 +870,9 @@ struct mprof_ctx {
   bool rowconst = true;
   // pinned host copy of the operand pairs the window launches pass as kernel parameters, valid
   // for operand generation rc_host_gen of device array rc_host_src (prepare_operands bumps op_gen)
-  double2* rc_host = nullptr;
-  size_t rc_host_cap = 0;
-  const double2* rc_host_src = nullptr;
+  void* rc_host = nullptr;
+  size_t rc_host_cap = 0;          // bytes
+  const void* rc_host_src = nullptr;
   unsigned long long rc_host_gen = 0, op_gen = 1;
   // z-norm statistics currently held in the workspace (series pointer, n, m, threshold)
   const double* stats_t = nullptr;
@@ -927,7 +927,7 @@ struct mprof_plan {
   long long ntiles = 0, n_near = 0, n_legacy = 0, R = 0;
   std::vector<mpg::RcBand> bands;  // constant-row part of the tile table
   int rc_policy = -1;
-  double2* host_pairs = nullptr;   // owned pinned mirror of the operand pairs (constant-row sweep)
+  void* host_pairs = nullptr;      // owned pinned mirror of the operand pairs (constant-row sweep)
   mpg::RcGraph rc_graph;           // the captured window chain
   bool aamp_cov = false, zn_colscale = false, wide = false, dense = false;
   unsigned long long probe_replays = 0;
@@ -1521,8 +1521,13 @@ int32_t probe_form(mprof_ctx* c, bool zn, const SweepParams& prm, int kb_lo, uin
 // forms whose rows per tile are whole windows.
 int rc_policy_of(const mprof_ctx* c, const mprof_config* cfg, long long R) {
   // (anytime sweeps run many small chunks: the legacy kernel's single launch per chunk)
-  if (!c->rowconst || cfg->exact || cfg->precision != MPROF_FP64 || c->dense || c->progress) return -1;
+  if (!c->rowconst || cfg->exact || c->dense || c->progress) return -1;
   if (R <= 0) return -1;
+  // FP32 mode: the covariance-only z-norm kernel (FFMA R, R, UR, R); the FP32 AAMP kernel is the
+  // (delta, sigma) slide with in-loop value keys and keeps the tile kernel
+  if (cfg->precision == MPROF_FP32)
+    return (cfg->family == MPROF_ZNORMALIZED && !c->zn_colscale) ? mpg::kRcZnormF32 : -1;
+  if (cfg->precision != MPROF_FP64) return -1;
   // Every covariance-only form: the replay-heavy ones (hit groups of 2, e.g. C5) stash their
   // accumulators per hit group, so a deferred replay restarts at its own group (sweep_rc.cu):
   // C5 2100 -> 1805 ms, random walk n = 2^20, m = 512 ACAMP 131.7 -> 114.4 ms; small sweeps
@@ -1535,16 +1540,16 @@ int rc_policy_of(const mprof_ctx* c, const mprof_config* cfg, long long R) {
 }
 
 // Pinned host mirror of `pairs` (count entries), refreshed when the operands were rebuilt.
-int32_t rc_host_pairs(mprof_ctx* c, const double2* pairs, size_t count, const double2** out) {
-  if (c->rc_host_src != pairs || c->rc_host_gen != c->op_gen || c->rc_host_cap < count) {
-    if (c->rc_host_cap < count) {
+int32_t rc_host_pairs(mprof_ctx* c, const void* pairs, size_t bytes, const void** out) {
+  if (c->rc_host_src != pairs || c->rc_host_gen != c->op_gen || c->rc_host_cap < bytes) {
+    if (c->rc_host_cap < bytes) {
       if (c->rc_host) cudaFreeHost(c->rc_host);
       c->rc_host = nullptr;
       c->rc_host_cap = 0;
-      CK(cudaMallocHost(&c->rc_host, count * sizeof(double2)));
-      c->rc_host_cap = count;
+      CK(cudaMallocHost(&c->rc_host, bytes));
+      c->rc_host_cap = bytes;
     }
-    CK(cudaMemcpyAsync(c->rc_host, pairs, count * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->rc_host, pairs, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->rc_host_src = pairs;
     c->rc_host_gen = c->op_gen;
@@ -1559,12 +1564,13 @@ int32_t rc_host_pairs(mprof_ctx* c, const double2* pairs, size_t count, const do
 int32_t dispatch_sweep(mprof_ctx* c, const mprof_config* cfg, const SweepParams& prm,
                        long long ntiles, long long n_near, long long n_legacy,
                        const std::vector<mpg::RcBand>& bands, int rc_policy,
-                       const double2* host_pairs, int k1, bool first_diag, uint32_t* launches,
+                       const void* host_pairs, int k1, bool first_diag, uint32_t* launches,
                        float* ms, uint32_t* rc_launches, mpg::RcGraph* rc_graph = nullptr) {
   int32_t st = MPROF_OK;
   if (n_legacy < ntiles && !host_pairs) {  // before the timed region: the mirror needs a sync
     if (rc_policy < 0 || bands.empty()) return fail(MPROF_E_CUDA, "internal: row bands without a kernel");
-    st = rc_host_pairs(c, mpg::rc_pairs(rc_policy, prm), (size_t)std::max(prm.L - 1, 1), &host_pairs);
+    st = rc_host_pairs(c, mpg::rc_pairs(rc_policy, prm),
+                       (size_t)std::max(prm.L - 1, 1) * mpg::rc_pair_bytes(rc_policy), &host_pairs);
     if (st != MPROF_OK) return st;
   }
   if (first_diag && !cfg->exact) {
@@ -2918,12 +2924,13 @@ int32_t mprof_plan_create(mprof_ctx* in, const double* d_t, uint64_t n64, const 
     if (!P->bands.empty()) {  // the window launches' row operands: one host mirror per plan
       const SweepParams pp = make_params(c, d_t, n, cfg, w, L, L);
       const size_t cnt = (size_t)std::max(L - 1, 1);
-      if (cudaMallocHost(&P->host_pairs, cnt * sizeof(double2)) != cudaSuccess) {
+      const size_t pbytes = cnt * mpg::rc_pair_bytes(P->rc_policy);
+      if (cudaMallocHost(&P->host_pairs, pbytes) != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(MPROF_E_OOM, "plan operand mirror"));
       }
       const cudaError_t e = cudaMemcpyAsync(P->host_pairs, mpg::rc_pairs(P->rc_policy, pp),
-                                            cnt * sizeof(double2), cudaMemcpyDeviceToHost, c->stream);
+                                            pbytes, cudaMemcpyDeviceToHost, c->stream);
       if (e != cudaSuccess) return bail(cuda_fail(e, "plan operand mirror"));
     }
     if (!tl.empty()) {

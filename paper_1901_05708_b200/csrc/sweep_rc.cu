@@ -118,16 +118,16 @@ template <class P, int D, int T, int S, bool GUARD>
 __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int X0,
                                              typename P::V (&acc)[D], int i0, int cnt, int kt,
                                              int kend, int L, BestEntry* best, double p,
-                                             unsigned long long* stats, const double2* crow,
-                                             int& ci, const typename P::V2* rowA_g, int svz,
-                                             double* gstash) {
+                                             unsigned long long* stats,
+                                             const typename P::V2* crow, int& ci,
+                                             const typename P::V2* rowA_g, int svz,
+                                             typename P::V* gstash) {
   using G = Geo<D, T, S>;
   using V2 = typename P::V2;
   using SMT = SweepSmem<P, D, T, S, false>;
   SMT& sm = rsm.base;
   constexpr bool EQ = SMT::EQ;
   static_assert(SMT::ZQ || SMT::EQ, "constant-row sweep: covariance-only filters");
-  static_assert(sizeof(typename P::V) == 8, "constant-row sweep: FP64");
   constexpr int HG = hit_group_for<P>();
   constexpr int SUP = rc_super_of<P>();      // blocks per stash
   static_assert(SUP % HG == 0 && S % (SUP * D) == 0, "super-groups are whole hit groups");
@@ -160,7 +160,8 @@ __device__ __forceinline__ void run_stage_rc(RcSmem<P, D, T, S>& rsm, int b, int
   const float2* zct = &sm.zcol[EQ ? 0 : threadIdx.x];
   const float4* ert = &sm.erow[0];
   const float2* zrt = &sm.zrow[0];
-  double* stash = (MPROF_RC_STASH_GLOBAL ? gstash : rsm.stash) + threadIdx.x;
+  using V = typename P::V;
+  V* stash = (MPROF_RC_STASH_GLOBAL ? gstash : reinterpret_cast<V*>(rsm.stash)) + threadIdx.x;
   unsigned hmask = 0;  // bit (sg * GPS + group): the group passed its block bounds
   int theta_nx;
   if constexpr (EQ) theta_nx = theta_e(ert[0], ect[0]);
@@ -282,7 +283,8 @@ __global__ void __launch_bounds__(T, MINB)
     if (threadIdx.x == 0) g_cell_ctx = CellCtx{prm.S, prm.mu, static_cast<double>(m)};
     __syncthreads();
   }
-  double* carry = rc.acc + (static_cast<size_t>(blockIdx.x) * G::K + threadIdx.x * D);
+  // (the carry and the stash are sized for doubles; the FP32 policy uses the front of each part)
+  V* carry = reinterpret_cast<V*>(rc.acc) + (static_cast<size_t>(blockIdx.x) * G::K + threadIdx.x * D);
   V acc[D];
   if (rc.w == 0) {
     // ---- seed (FP64): direct length-m sum for the pair (ra, ra + kt + d), as sweep_kernel ----
@@ -349,18 +351,13 @@ __global__ void __launch_bounds__(T, MINB)
     if (steps <= 0) return;
     __syncthreads();  // seed scratch reuse
   } else {
-    const double2* cp = reinterpret_cast<const double2*>(carry);
 #pragma unroll
-    for (int d = 0; d < D; d += 2) {
-      const double2 v = __ldcg(cp + d / 2);
-      acc[d] = v.x;
-      acc[d + 1] = v.y;
-    }
+    for (int d = 0; d < D; ++d) acc[d] = __ldcg(carry + d);
   }
 
   // ---- the CTA's replay stash: a slot of the per-SM pool (claimed in the SM's bitmap, released
   // at the end; the pool has more slots per SM than CTAs can be resident) ----
-  double* gstash = nullptr;
+  V* gstash = nullptr;
   if constexpr (MPROF_RC_STASH_GLOBAL) {
     __shared__ int s_slot;
     if (threadIdx.x == 0) {
@@ -376,7 +373,7 @@ __global__ void __launch_bounds__(T, MINB)
       s_slot = static_cast<int>(smid) * kRcSmSlots + got;
     }
     __syncthreads();
-    gstash = rc.stash + static_cast<size_t>(s_slot) * rc_stash_doubles<P, D, T, S>();
+    gstash = reinterpret_cast<V*>(rc.stash) + static_cast<size_t>(s_slot) * rc_stash_doubles<P, D, T, S>();
   }
 
   // ---- stage pipeline over the window's row transitions (sweep_kernel's, rows from rc.rows) --
@@ -398,10 +395,12 @@ __global__ void __launch_bounds__(T, MINB)
     const bool full = (cnt == S) && (kb + G::K <= kend) && (i0 + cnt + kb + G::K - 1 <= L - 1);
     if (full) {
       run_stage_rc<P, D, T, S, false>(rsm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p,
-                                      prm.stats, rc.rows, ci, A + i0, rc.zero, gstash);
+                                      prm.stats, reinterpret_cast<const typename P::V2*>(rc.rows), ci,
+                                      A + i0, rc.zero, gstash);
     } else {
       run_stage_rc<P, D, T, S, true>(rsm, st & 1, s0, acc, i0, cnt, kt, kend, L, prm.best, prm.p,
-                                     prm.stats, rc.rows, ci, A + i0, rc.zero, gstash);
+                                     prm.stats, reinterpret_cast<const typename P::V2*>(rc.rows), ci,
+                                      A + i0, rc.zero, gstash);
     }
     if (st + 1 == nst) break;
     cp_async_wait<0>();
@@ -416,15 +415,14 @@ __global__ void __launch_bounds__(T, MINB)
     if (threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      const int bsl = (static_cast<int>((gstash - rc.stash) / rc_stash_doubles<P, D, T, S>())) % kRcSmSlots;
+      const int bsl = (static_cast<int>((gstash - reinterpret_cast<V*>(rc.stash)) / rc_stash_doubles<P, D, T, S>())) % kRcSmSlots;
       atomicAnd(&rc.stash_bits[smid], ~(1u << bsl));
     }
   }
   // more transitions of this tile follow in the next window: carry the accumulators
   if (left > kRcW) {
-    double2* cp = reinterpret_cast<double2*>(carry);
 #pragma unroll
-    for (int d = 0; d < D; d += 2) __stcg(cp + d / 2, make_double2(acc[d], acc[d + 1]));
+    for (int d = 0; d < D; ++d) __stcg(carry + d, acc[d]);
   }
 }
 
@@ -451,6 +449,7 @@ auto with_rc_policy(int policy, F&& f) {
     case kRcZnorm: return f.template operator()<Znorm<false>>();
     case kRcWideZnorm: return f.template operator()<Wide<Znorm<false>>>();
     case kRcEuclidCov: return f.template operator()<EuclidCov>();
+    case kRcZnormF32: return f.template operator()<ZnormF32<false>>();
     default: return f.template operator()<Wide<EuclidCov>>();
   }
 #endif
@@ -517,7 +516,7 @@ namespace {
 // chain streams, join back into `main`.
 template <class P>
 cudaError_t rc_issue(const SweepParams& prm, const std::vector<RcBand>& bands, RcRes& res,
-                     cudaStream_t main, const double2* host_pairs, size_t per_tile,
+                     cudaStream_t main, const unsigned char* host_pairs, size_t per_tile,
                      uint32_t* launches) {
   auto kern = rc_kernel<P>();
   const size_t smem = rc_smem<P>();
@@ -550,7 +549,9 @@ cudaError_t rc_issue(const SweepParams& prm, const std::vector<RcBand>& bands, R
       if (nt <= 0) continue;
       const long long r0 = (long long)bd.ra + (long long)w * kRcW;
       const long long rows = std::min<long long>(kRcW, (long long)prm.L - 1 - r0);
-      if (rows > 0) std::memcpy(rc.rows, host_pairs + r0, (size_t)rows * sizeof(double2));
+      if (rows > 0)
+        std::memcpy(rc.rows, host_pairs + (size_t)r0 * sizeof(typename P::V2),
+                    (size_t)rows * sizeof(typename P::V2));
       SweepParams q = prm;
       q.tiles = prm.tiles + bd.off;
       rc.w = w;
@@ -571,9 +572,12 @@ cudaError_t rc_issue(const SweepParams& prm, const std::vector<RcBand>& bands, R
 
 }  // namespace
 
-const double2* rc_pairs(int policy, const SweepParams& prm) {
+const void* rc_pairs(int policy, const SweepParams& prm) {
+  if (policy == kRcZnormF32) return prm.A32;
   return (policy == kRcEuclidCov || policy == kRcWideEuclidCov) ? prm.A2 : prm.A;
 }
+
+size_t rc_pair_bytes(int policy) { return policy == kRcZnormF32 ? sizeof(float2) : sizeof(double2); }
 
 void rc_graph_release(RcGraph& g) {
   if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -581,8 +585,9 @@ void rc_graph_release(RcGraph& g) {
 }
 
 cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBand>& bands,
-                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches,
+                     RcRes& res, cudaStream_t main, const void* host_pairs_v, uint32_t* launches,
                      RcGraph* graph) {
+  const unsigned char* host_pairs = static_cast<const unsigned char*>(host_pairs_v);
   if (bands.empty()) return cudaSuccess;
   size_t most = 0;
   for (const RcBand& bd : bands)

@@ -51,7 +51,9 @@ constexpr int kRcSlots = MPROF_RC_CHAINS;
 constexpr int kRcSmSlots = 4;   // stash slots per SM (>= resident CTAs per SM: 3)
 static_assert(kRcW * 16 <= 30720, "the row window must fit the kernel parameter space");
 
-enum RcPolicy { kRcZnorm = 0, kRcWideZnorm = 1, kRcEuclidCov = 2, kRcWideEuclidCov = 3 };
+// (kRcZnormF32: the FP32 mode's covariance-only z-norm kernel; its FFMAs take the row operand from
+// a uniform register the same way)
+enum RcPolicy { kRcZnorm = 0, kRcWideZnorm = 1, kRcEuclidCov = 2, kRcWideEuclidCov = 3, kRcZnormF32 = 4 };
 
 // One row band of the tile grid: the tiles that start at row `ra` (ascending first diagonal, so
 // their row ends are non-increasing and the tiles still alive in window w are a prefix), at
@@ -105,11 +107,13 @@ int rc_blocks_per_sm(int policy);
 // graph != nullptr: replay (or first capture) the chain as a CUDA graph; falls back to direct
 // launches when the stream cannot be captured.
 cudaError_t rc_sweep(int policy, const SweepParams& prm, const std::vector<RcBand>& bands,
-                     RcRes& res, cudaStream_t main, const double2* host_pairs, uint32_t* launches,
+                     RcRes& res, cudaStream_t main, const void* host_pairs, uint32_t* launches,
                      RcGraph* graph = nullptr);
 
 // Device pointer of the policy's operand pairs in prm (what host_pairs must mirror).
-const double2* rc_pairs(int policy, const SweepParams& prm);
+const void* rc_pairs(int policy, const SweepParams& prm);
+// Bytes of one operand pair of the policy (double2, or float2 in FP32 mode).
+size_t rc_pair_bytes(int policy);
 
 void rc_release(RcRes& res);
 

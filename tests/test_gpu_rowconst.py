@@ -89,3 +89,21 @@ def test_row_const_replay_heavy_series_bit_identical(family):
     assert a.info.row_windows > 0 and b.info.row_windows == 0
     np.testing.assert_array_equal(a.nn_index, b.nn_index)
     np.testing.assert_array_equal(a.distances.view(np.uint64), b.distances.view(np.uint64))
+
+
+def test_row_const_fp32_znorm_bit_identical(series):
+    """FP32 mode, covariance-only z-norm kernel: the constant-row path (float accumulators, float
+    row operands in the parameter space, float carry and stash) against the tile kernel."""
+    out = []
+    for rc in (1, 0):
+        ctx = mp.Context(0)
+        ctx.set_row_const(rc)
+        cfg = mp.ProfileConfig(M, mp.DistanceKind.znormalized())
+        cfg.precision = mp.Precision.FP32
+        out.append(mp.acamp(mp.make_time_series(series), cfg, ctx=ctx))
+        ctx.close()
+    a, b = out
+    assert a.info.policy == b.info.policy == "ZnormF32<0>"
+    assert a.info.row_windows > 0 and b.info.row_windows == 0
+    np.testing.assert_array_equal(a.nn_index, b.nn_index)
+    np.testing.assert_array_equal(a.distances.view(np.uint64), b.distances.view(np.uint64))
