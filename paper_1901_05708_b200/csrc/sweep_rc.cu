@@ -351,8 +351,18 @@ __global__ void __launch_bounds__(T, MINB)
     if (steps <= 0) return;
     __syncthreads();  // seed scratch reuse
   } else {
+    if constexpr (sizeof(V) == 8) {  // 16-byte loads
+      const double2* cp = reinterpret_cast<const double2*>(carry);
 #pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] = __ldcg(carry + d);
+      for (int d = 0; d < D; d += 2) {
+        const double2 v = __ldcg(cp + d / 2);
+        acc[d] = v.x;
+        acc[d + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[d] = __ldcg(carry + d);
+    }
   }
 
   // ---- the CTA's replay stash: a slot of the per-SM pool (claimed in the SM's bitmap, released
@@ -421,8 +431,14 @@ __global__ void __launch_bounds__(T, MINB)
   }
   // more transitions of this tile follow in the next window: carry the accumulators
   if (left > kRcW) {
+    if constexpr (sizeof(V) == 8) {
+      double2* cp = reinterpret_cast<double2*>(carry);
 #pragma unroll
-    for (int d = 0; d < D; ++d) __stcg(carry + d, acc[d]);
+      for (int d = 0; d < D; d += 2) __stcg(cp + d / 2, make_double2(acc[d], acc[d + 1]));
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) __stcg(carry + d, acc[d]);
+    }
   }
 }
 
